@@ -1,0 +1,173 @@
+/*
+ * bsrprune.h -- C ABI of the B200 (sm_100a) hot path of structured activation
+ * pruning, arXiv 2311.16883 (Barley & Froening).
+ *
+ * What the path computes (/root/reference/PAPER.md, cited as P:L<line>):
+ *   forward  : every saved linear-layer activation X (M x K, rows =
+ *              batch x tokens, row-major) is tiled into b x b blocks; the l2
+ *              norm of every block is computed, the k largest-norm blocks are
+ *              kept, the others are zeroed, and the result is stored in Block
+ *              Sparse Row form (fig:operator
+ *              P:L313-321, BSR P:L159-170).
+ *   backward : the weight gradient dW = X_bsr^T . dY is a block-sparse x dense
+ *              product over the kept blocks only; dX stays dense
+ *              and is not part of this library.
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  * Pointers are CUDA DEVICE pointers unless marked (host).  The caller owns
+ *    every buffer; the library never allocates, frees or synchronises.
+ *  * Device work is enqueued on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream) and is asynchronous: results are valid once
+ *    the stream reaches that point.  Asynchronous device faults surface at the
+ *    caller's next synchronisation.  No call performs a device->host copy, so
+ *    every call is CUDA-graph capturable.
+ *  * Arguments are validated on the host before anything is enqueued; on any
+ *    non-BSR_OK return nothing has been written.  bsr_last_error() then holds a
+ *    human-readable reason for the calling thread.
+ *  * Block flat index: f = I * (K/b) + J for block row I < M/b and block
+ *    column J < K/b.
+ *  * Element types: BSR_DT_F32 (IEEE binary32) and BSR_DT_BF16 (bfloat16).
+ *  * Supported block edges: b in {4, 8, 16, 32, 64}; b must divide M and K.
+ *    Base pointers must be 16-byte aligned and K * sizeof(elem) a multiple of
+ *    16 bytes (vectorised rows).
+ *  * The library is reentrant; the only global state is the thread-local
+ *    error string and per-device kernel attributes set once.
+ */
+#ifndef BSRPRUNE_H
+#define BSRPRUNE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BSR_API __attribute__((visibility("default")))
+#else
+#define BSR_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BSR_OK = 0,
+    BSR_ERR_INVALID_ARG = 1, /* null pointer, keep outside [0,1] or NaN, k > N, bad enum */
+    BSR_ERR_SHAPE = 2,       /* M, K <= 0, b does not divide M or K, size overflow      */
+    BSR_ERR_UNSUPPORTED = 3, /* b not in {4,8,16,32,64}, dtype/precision combination    */
+    BSR_ERR_ALIGNMENT = 4,   /* pointer or row pitch not 16-byte aligned                */
+    BSR_ERR_WORKSPACE = 5,   /* workspace null or smaller than the size query           */
+    BSR_ERR_CUDA = 6         /* a CUDA launch failed; bsr_last_error() has the string   */
+} bsr_status_t;
+
+typedef enum { BSR_DT_F32 = 0, BSR_DT_BF16 = 1 } bsr_dtype_t;
+
+/* Arithmetic of bsr_wgrad (reading R9 in DESIGN.md):
+ *   BSR_PREC_FP32 : fp32 operands, fp32 FFMA with round-to-nearest, fixed
+ *                   summation order (deterministic).  Graded at relative
+ *                   Frobenius error <= 1e-5 against the fp64 oracle.
+ *   BSR_PREC_TF32 : tcgen05 tensor cores, kind::tf32 on fp32 operands, fp32
+ *                   accumulation in TMEM.  Graded at <= 5e-3.
+ *   BSR_PREC_BF16 : tcgen05 tensor cores, kind::f16 on bf16 operands (X values
+ *                   and dY both bf16), fp32 accumulation in TMEM.  <= 5e-3. */
+typedef enum { BSR_PREC_FP32 = 0, BSR_PREC_TF32 = 1, BSR_PREC_BF16 = 2 } bsr_prec_t;
+
+/* A Block Sparse Row matrix.  The struct itself lives in host
+ * memory; the three arrays are device memory owned by the caller.
+ *   rowptr [M/b + 1]  int32: rowptr[0] = 0, rowptr[I+1] - rowptr[I] = stored
+ *                     blocks in block row I ("crow");
+ *                     rowptr[M/b] = nnzb.
+ *   colidx [nnzb]     int32: block column of each stored block, strictly
+ *                     increasing inside a block row ("col").
+ *   values [nnzb][b][b] elements of `dtype`, one block after another in
+ *                     (block row, colidx) order, row-major inside a block,
+ *                     bit-exact copies of X (reading R7). */
+typedef struct {
+    int64_t M, K;     /* logical dense shape                        */
+    int32_t b;        /* square block edge                          */
+    int32_t dtype;    /* bsr_dtype_t of values                      */
+    int64_t nnzb;     /* stored blocks (== k after bsr_prune)       */
+    int32_t *rowptr;
+    int32_t *colidx;
+    void *values;
+} bsr_t;
+
+/* ---- host-only pure helpers (no CUDA calls) ------------------------------ */
+
+/* N = (M/b) * (K/b); -1 if the shape is invalid or b does not divide M, K. */
+BSR_API int64_t bsr_num_blocks(int64_t M, int64_t K, int32_t b);
+
+/* Kept blocks for keep ratio keep = 1 - s: k = floor(keep * N + 0.5), clamped
+ * to [0, N] ("k is determined by multiplying the total number of
+ * blocks N by the sparsity parameter s"; nearest rounding pinned by Table II,
+ * P:L180-197).  -1 if keep is NaN or outside [0, 1] or N < 0. */
+BSR_API int64_t bsr_keep_count(int64_t nblocks, double keep);
+
+/* Stored bytes of the BSR: k*b*b*sizeof(dtype) + 4*k + 4*(M/b + 1)
+ * (BJ closed form with 4-byte values).  0 on invalid input. */
+BSR_API size_t bsr_storage_bytes(int64_t M, int32_t b, int64_t k, int32_t dtype);
+
+/* Device workspace (bytes) bsr_prune / bsr_prune_k need for this shape.
+ * 0 on invalid input.  The workspace need not be initialised. */
+BSR_API size_t bsr_prune_workspace_bytes(int64_t M, int64_t K, int32_t b);
+
+/* Device workspace (bytes) bsr_wgrad needs.  0 means none is needed (a NULL
+ * workspace is then accepted). */
+BSR_API size_t bsr_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec);
+
+/* ---- device work ------------------------------------------------------------ */
+
+/* Prune X (M x K, row-major, `dtype`) to its top-k blocks by l2 norm and pack
+ * them into BSR:
+ *   1. sumsq[f] = sum of squares of block f in fp32 (fixed summation tree);
+ *      ranking by sumsq equals ranking by the l2 norm sqrt(sumsq).
+ *   2. keep the k blocks with the largest sumsq, k = bsr_keep_count(N, keep);
+ *      among equal sumsq the lower flat index is kept first (BJ tie rule).
+ *   3. write out->rowptr, out->colidx, out->values (layout above).
+ * `out` (host struct): rowptr/colidx/values must point to caller-allocated
+ * device arrays of sizes M/b+1, k and k*b*b elements; on success the call
+ * fills out->M, K, b, dtype and sets out->nnzb = k.  values/colidx may be NULL
+ * iff k == 0.  X must not overlap any output.  ws must hold
+ * bsr_prune_workspace_bytes(M, K, b) bytes. */
+BSR_API bsr_status_t bsr_prune(const void *X, int64_t M, int64_t K, int32_t b, double keep,
+                       int32_t dtype, bsr_t *out, void *ws, size_t ws_bytes, void *stream);
+
+/* As bsr_prune with an explicit number of kept blocks k in [0, N]. */
+BSR_API bsr_status_t bsr_prune_k(const void *X, int64_t M, int64_t K, int32_t b, int64_t k,
+                         int32_t dtype, bsr_t *out, void *ws, size_t ws_bytes, void *stream);
+
+/* Test hook for step 1 alone: sumsq[N] (fp32, flat order) of every b x b block
+ * of X, computed by the same kernel code as bsr_prune. */
+BSR_API bsr_status_t bsr_block_sumsq(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype,
+                             float *sumsq, void *stream);
+
+/* Dense M x K matrix (A->dtype) with every stored block at its position and
+ * +0.0 elsewhere: X_out == X masked to the kept blocks, bit for bit
+ * (SPEC decode; P:L162-168 read backwards).  X_out must hold M*K elements. */
+BSR_API bsr_status_t bsr_decompress(const bsr_t *A, void *X_out, void *stream);
+
+/* Weight gradient (BJ):
+ *   dW[J*b + c][n] (+)= sum over stored blocks (I, J), sum over r < b of
+ *                       values(I,J)[r][c] * dY[I*b + r][n]
+ * i.e. dW = X_bsr^T . dY with dW K x N row-major fp32 and dY M x N row-major of
+ * `dy_dtype`.  accumulate = 0 overwrites dW, 1 adds to it.  Block rows and
+ * blocks that were pruned contribute nothing and are never read.  `prec`
+ * selects the arithmetic (see bsr_prec_t): FP32 accepts f32 or bf16 operands;
+ * TF32 needs f32 values and f32 dY; BF16 needs bf16 values and bf16 dY, b in
+ * {16, 32, 64} and N a multiple of 128 for the tensor-core paths. */
+BSR_API bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dW,
+                       int32_t accumulate, int32_t prec, void *ws, size_t ws_bytes, void *stream);
+
+/* Static description of a status code. */
+BSR_API const char *bsr_status_string(int32_t status);
+
+/* Detail of the calling thread's last failing call ("" if none). */
+BSR_API const char *bsr_last_error(void);
+
+/* Library version string, e.g. "bsrprune 0.1.0 sm_100a". */
+BSR_API const char *bsr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSRPRUNE_H */

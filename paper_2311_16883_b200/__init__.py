@@ -1,0 +1,172 @@
+"""B200-native hot path of structured activation pruning (arXiv 2311.16883).
+
+Thin Python layer over the C-ABI library ``libbsrprune.so`` (include/bsrprune.h).
+PyTorch supplies device memory and the current CUDA stream only; every step --
+block norms, top-k, BSR packing, decompression and the block-sparse weight
+gradient -- runs in the library's hand-written sm_100a kernels.
+
+    bsr = prune(X, b=32, keep=0.5)          # forward: X (M x K, cuda) -> BSR
+    dW  = wgrad(bsr, dY, prec="fp32")       # backward: dW = X_bsr^T . dY (K x N)
+    Xm  = decompress(bsr)                   # X masked to the kept blocks
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import BsrError, DT_BF16, DT_F32, PREC
+
+__all__ = ["BSR", "BsrError", "prune", "decompress", "wgrad", "block_sumsq", "num_blocks", "keep_count",
+           "storage_bytes", "workspace", "version"]
+
+_DT = {torch.float32: DT_F32, torch.bfloat16: DT_BF16}
+
+
+def _dt(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t.dtype} (float32 or bfloat16)") from None
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _cuda2d(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dim() != 2 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous 2-D tensor")
+    return t
+
+
+@dataclass
+class BSR:
+    """Block Sparse Row matrix: device tensors + logical shape."""
+    rowptr: torch.Tensor   # int32 [M/b + 1]
+    colidx: torch.Tensor   # int32 [nnzb]
+    values: torch.Tensor   # dtype [nnzb, b, b]
+    M: int
+    K: int
+    b: int
+
+    @property
+    def nnzb(self) -> int:
+        return self.colidx.numel()
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.values.dtype
+
+    def nbytes(self) -> int:
+        return storage_bytes(self.M, self.b, self.nnzb, self.dtype)
+
+    def c_struct(self) -> _lib.BsrT:
+        return _lib.BsrT(self.M, self.K, self.b, _dt(self.values), self.nnzb, self.rowptr.data_ptr(),
+                         self.colidx.data_ptr() if self.nnzb else None,
+                         self.values.data_ptr() if self.nnzb else None)
+
+
+def version() -> str:
+    return _lib.load().bsr_version().decode()
+
+
+def num_blocks(M: int, K: int, b: int) -> int:
+    return int(_lib.load().bsr_num_blocks(M, K, b))
+
+
+def keep_count(N: int, keep: float) -> int:
+    k = int(_lib.load().bsr_keep_count(N, float(keep)))
+    if k < 0:
+        raise ValueError("keep must be in [0, 1]")
+    return k
+
+
+def storage_bytes(M: int, b: int, k: int, dtype=torch.float32) -> int:
+    return int(_lib.load().bsr_storage_bytes(M, b, k, _DT[dtype]))
+
+
+_WS: dict = {}
+
+
+def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    """Cached device workspace of at least nbytes (one per device)."""
+    key = (device.type, device.index)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
+
+
+def alloc_bsr(M: int, K: int, b: int, k: int, dtype: torch.dtype, device) -> BSR:
+    return BSR(rowptr=torch.empty(M // b + 1, dtype=torch.int32, device=device),
+               colidx=torch.empty(k, dtype=torch.int32, device=device),
+               values=torch.empty((k, b, b), dtype=dtype, device=device), M=M, K=K, b=b)
+
+
+def prune(X: torch.Tensor, b: int, keep: float | None = None, k: int | None = None, out: BSR | None = None,
+          stream=None) -> BSR:
+    """Keep the top-k b x b blocks of X by l2 norm and pack them into BSR.
+
+    Exactly one of ``keep`` (ratio, k = nearest(keep*N)) or ``k`` is given."""
+    lib = _lib.load()
+    X = _cuda2d(X, "X")
+    M, K = X.shape
+    N = num_blocks(M, K, b)
+    if N < 0:
+        raise _lib.BsrError(2, f"b={b} must divide M={M} and K={K}")
+    if (keep is None) == (k is None):
+        raise ValueError("give exactly one of keep or k")
+    if k is None:
+        k = keep_count(N, keep)
+    out = out or alloc_bsr(M, K, b, k, X.dtype, X.device)
+    ws_bytes = lib.bsr_prune_workspace_bytes(M, K, b)
+    ws = workspace(ws_bytes, X.device)
+    cs = out.c_struct()
+    _lib.check(lib.bsr_prune_k(X.data_ptr(), M, K, b, k, _dt(X), ctypes.byref(cs), ws.data_ptr(), ws.numel(),
+                               _stream(stream)))
+    return out
+
+
+def block_sumsq(X: torch.Tensor, b: int, stream=None) -> torch.Tensor:
+    lib = _lib.load()
+    X = _cuda2d(X, "X")
+    M, K = X.shape
+    N = num_blocks(M, K, b)
+    out = torch.empty(max(N, 0), dtype=torch.float32, device=X.device)
+    _lib.check(lib.bsr_block_sumsq(X.data_ptr(), M, K, b, _dt(X), out.data_ptr(), _stream(stream)))
+    return out
+
+
+def decompress(A: BSR, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    lib = _lib.load()
+    out = torch.empty((A.M, A.K), dtype=A.dtype, device=A.rowptr.device) if out is None else out
+    cs = A.c_struct()
+    _lib.check(lib.bsr_decompress(ctypes.byref(cs), out.data_ptr(), _stream(stream)))
+    return out
+
+
+def wgrad(A: BSR, dY: torch.Tensor, prec: str = "fp32", out: torch.Tensor | None = None,
+          accumulate: bool = False, stream=None) -> torch.Tensor:
+    """dW = X_bsr^T . dY (K x N fp32) over the kept blocks only."""
+    lib = _lib.load()
+    dY = _cuda2d(dY, "dY")
+    if dY.shape[0] != A.M:
+        raise ValueError(f"dY has {dY.shape[0]} rows, BSR has M={A.M}")
+    N = dY.shape[1]
+    if out is None:
+        out = torch.empty((A.K, N), dtype=torch.float32, device=dY.device)
+    p = PREC[prec]
+    ws_bytes = lib.bsr_wgrad_workspace_bytes(A.M, A.K, A.b, N, p)
+    ws = workspace(ws_bytes, dY.device) if ws_bytes else None
+    cs = A.c_struct()
+    _lib.check(lib.bsr_wgrad(ctypes.byref(cs), dY.data_ptr(), _dt(dY), N, out.data_ptr(), int(accumulate), p,
+                             ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0,
+                             _stream(stream)))
+    return out

@@ -1,0 +1,78 @@
+"""ctypes binding of libbsrprune.so (include/bsrprune.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels.  There is no
+CPU or PyTorch fallback: if the shared library is missing or was built for
+another architecture the import / first call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libbsrprune.so")
+
+BSR_OK = 0
+STATUS_NAMES = {0: "BSR_OK", 1: "BSR_ERR_INVALID_ARG", 2: "BSR_ERR_SHAPE", 3: "BSR_ERR_UNSUPPORTED",
+                4: "BSR_ERR_ALIGNMENT", 5: "BSR_ERR_WORKSPACE", 6: "BSR_ERR_CUDA"}
+DT_F32, DT_BF16 = 0, 1
+PREC = {"fp32": 0, "tf32": 1, "bf16": 2}
+
+EXPORTED = ["bsr_num_blocks", "bsr_keep_count", "bsr_storage_bytes", "bsr_prune_workspace_bytes",
+            "bsr_wgrad_workspace_bytes", "bsr_prune", "bsr_prune_k", "bsr_block_sumsq", "bsr_decompress",
+            "bsr_wgrad", "bsr_status_string", "bsr_last_error", "bsr_version"]
+
+
+class BsrT(ctypes.Structure):
+    """Mirror of bsr_t."""
+    _fields_ = [("M", ctypes.c_int64), ("K", ctypes.c_int64), ("b", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("nnzb", ctypes.c_int64), ("rowptr", ctypes.c_void_p), ("colidx", ctypes.c_void_p),
+                ("values", ctypes.c_void_p)]
+
+
+class BsrError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {detail}")
+        self.status = status
+        self.detail = detail
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                           "(there is no fallback implementation)")
+    lib = ctypes.CDLL(path)
+    i64, i32, vp, sz, dbl = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_double
+    P = ctypes.POINTER(BsrT)
+    sig = {
+        "bsr_num_blocks": (i64, [i64, i64, i32]),
+        "bsr_keep_count": (i64, [i64, dbl]),
+        "bsr_storage_bytes": (sz, [i64, i32, i64, i32]),
+        "bsr_prune_workspace_bytes": (sz, [i64, i64, i32]),
+        "bsr_wgrad_workspace_bytes": (sz, [i64, i64, i32, i64, i32]),
+        "bsr_prune": (i32, [vp, i64, i64, i32, dbl, i32, P, vp, sz, vp]),
+        "bsr_prune_k": (i32, [vp, i64, i64, i32, i64, i32, P, vp, sz, vp]),
+        "bsr_block_sumsq": (i32, [vp, i64, i64, i32, i32, vp, vp]),
+        "bsr_decompress": (i32, [P, vp, vp]),
+        "bsr_wgrad": (i32, [P, vp, i32, i64, vp, i32, i32, vp, sz, vp]),
+        "bsr_status_string": (ctypes.c_char_p, [i32]),
+        "bsr_last_error": (ctypes.c_char_p, []),
+        "bsr_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int):
+    if status != BSR_OK:
+        raise BsrError(status, load().bsr_last_error().decode())

@@ -1,0 +1,237 @@
+// abi.cu -- the exported C ABI (include/bsrprune.h): host-side validation,
+// size queries, error reporting and dispatch to the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/bsrprune.h"
+#include "launch.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+bsr_status_t fail(bsr_status_t st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+bsr_status_t ok() {
+    g_last_error.clear();
+    return BSR_OK;
+}
+
+bsr_status_t cuda_status(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return ok();
+    return fail(BSR_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool supported_b(int32_t b) { return b == 4 || b == 8 || b == 16 || b == 32 || b == 64; }
+int elem_size(int32_t dt) { return dt == BSR_DT_F32 ? 4 : dt == BSR_DT_BF16 ? 2 : 0; }
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Byte ranges [a, a+na) and [b, b+nb) overlap.
+bool overlap(const void *a, size_t na, const void *b, size_t nb) {
+    if (!a || !b || na == 0 || nb == 0) return false;
+    auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+    return x < y + nb && y < x + na;
+}
+
+bsr_status_t check_shape(int64_t M, int64_t K, int32_t b, int32_t dtype) {
+    if (elem_size(dtype) == 0) return fail(BSR_ERR_INVALID_ARG, "dtype %d is not BSR_DT_F32 or BSR_DT_BF16", dtype);
+    if (!supported_b(b)) return fail(BSR_ERR_UNSUPPORTED, "block size b=%d not in {4,8,16,32,64}", b);
+    if (M <= 0 || K <= 0) return fail(BSR_ERR_SHAPE, "M=%lld and K=%lld must be positive", (long long)M, (long long)K);
+    if (M % b != 0 || K % b != 0)
+        return fail(BSR_ERR_SHAPE, "b=%d must divide M=%lld and K=%lld", b, (long long)M, (long long)K);
+    if ((K * elem_size(dtype)) % 16 != 0)
+        return fail(BSR_ERR_ALIGNMENT, "row pitch K*sizeof(elem)=%lld bytes is not a multiple of 16",
+                    (long long)(K * elem_size(dtype)));
+    const int64_t N = (M / b) * (K / b);
+    if (N >= (int64_t(1) << 31) || M / b >= (int64_t(1) << 31) || M > (int64_t(1) << 40) || K > (int64_t(1) << 30))
+        return fail(BSR_ERR_SHAPE, "shape too large (block count %lld must stay below 2^31)", (long long)N);
+    return BSR_OK;
+}
+
+bsr_status_t check_bsr(const bsr_t *A) {
+    if (!A) return fail(BSR_ERR_INVALID_ARG, "BSR descriptor is NULL");
+    bsr_status_t st = check_shape(A->M, A->K, A->b, A->dtype);
+    if (st != BSR_OK) return st;
+    const int64_t N = (A->M / A->b) * (A->K / A->b);
+    if (A->nnzb < 0 || A->nnzb > N)
+        return fail(BSR_ERR_INVALID_ARG, "nnzb=%lld outside [0, %lld]", (long long)A->nnzb, (long long)N);
+    if (!A->rowptr) return fail(BSR_ERR_INVALID_ARG, "rowptr is NULL");
+    if (A->nnzb > 0 && (!A->colidx || !A->values))
+        return fail(BSR_ERR_INVALID_ARG, "colidx/values are NULL with nnzb=%lld", (long long)A->nnzb);
+    if (A->values && !aligned16(A->values)) return fail(BSR_ERR_ALIGNMENT, "values is not 16-byte aligned");
+    return BSR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t bsr_num_blocks(int64_t M, int64_t K, int32_t b) {
+    if (M <= 0 || K <= 0 || b <= 0 || M % b != 0 || K % b != 0) return -1;
+    return (M / b) * (K / b);
+}
+
+int64_t bsr_keep_count(int64_t nblocks, double keep) {
+    if (nblocks < 0 || !(keep >= 0.0 && keep <= 1.0)) return -1;
+    int64_t k = (int64_t)std::floor(keep * (double)nblocks + 0.5);
+    return k < 0 ? 0 : (k > nblocks ? nblocks : k);
+}
+
+size_t bsr_storage_bytes(int64_t M, int32_t b, int64_t k, int32_t dtype) {
+    const int es = elem_size(dtype);
+    if (M <= 0 || b <= 0 || M % b != 0 || k < 0 || es == 0) return 0;
+    return (size_t)k * b * b * es + (size_t)k * 4 + (size_t)(M / b + 1) * 4;
+}
+
+size_t bsr_prune_workspace_bytes(int64_t M, int64_t K, int32_t b) {
+    const int64_t N = bsr_num_blocks(M, K, b);
+    if (N < 0 || !supported_b(b)) return 0;
+    return bsrp::prune_ws_layout(N).total;
+}
+
+size_t bsr_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec) {
+    if (bsr_num_blocks(M, K, b) < 0 || N <= 0) return 0;
+    if (prec == BSR_PREC_FP32) return 0;
+    return bsrp::wgrad_tc_ws_bytes(M, K, b, N);
+}
+
+static bsr_status_t prune_impl(const void *X, int64_t M, int64_t K, int32_t b, int64_t k, int32_t dtype,
+                               bsr_t *out, void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_shape(M, K, b, dtype);
+    if (st != BSR_OK) return st;
+    const int64_t N = (M / b) * (K / b);
+    if (k < 0 || k > N) return fail(BSR_ERR_INVALID_ARG, "k=%lld outside [0, N=%lld]", (long long)k, (long long)N);
+    if (!X) return fail(BSR_ERR_INVALID_ARG, "X is NULL");
+    if (!out) return fail(BSR_ERR_INVALID_ARG, "output BSR descriptor is NULL");
+    if (!out->rowptr) return fail(BSR_ERR_INVALID_ARG, "out->rowptr is NULL");
+    if (k > 0 && (!out->colidx || !out->values))
+        return fail(BSR_ERR_INVALID_ARG, "out->colidx / out->values are NULL with k=%lld", (long long)k);
+    if (!aligned16(X)) return fail(BSR_ERR_ALIGNMENT, "X is not 16-byte aligned");
+    if (k > 0 && !aligned16(out->values)) return fail(BSR_ERR_ALIGNMENT, "out->values is not 16-byte aligned");
+    const int es = elem_size(dtype);
+    const size_t xbytes = (size_t)M * K * es;
+    if (overlap(X, xbytes, out->values, (size_t)k * b * b * es) || overlap(X, xbytes, out->colidx, (size_t)k * 4) ||
+        overlap(X, xbytes, out->rowptr, (size_t)(M / b + 1) * 4))
+        return fail(BSR_ERR_INVALID_ARG, "X overlaps an output array");
+    const size_t need = bsrp::prune_ws_layout(N).total;
+    if (0 < k && k < N) {
+        if (!ws || ws_bytes < need)
+            return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+        if (!aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
+    }
+    cudaError_t e = bsrp::launch_prune(X, M, K, b, es, k, out->rowptr, out->colidx, out->values, ws,
+                                       static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_status(e, "bsr_prune launch");
+    out->M = M;
+    out->K = K;
+    out->b = b;
+    out->dtype = dtype;
+    out->nnzb = k;
+    return ok();
+}
+
+bsr_status_t bsr_prune(const void *X, int64_t M, int64_t K, int32_t b, double keep, int32_t dtype, bsr_t *out,
+                       void *ws, size_t ws_bytes, void *stream) {
+    if (!(keep >= 0.0 && keep <= 1.0)) return fail(BSR_ERR_INVALID_ARG, "keep=%g must be in [0, 1]", keep);
+    bsr_status_t st = check_shape(M, K, b, dtype);
+    if (st != BSR_OK) return st;
+    return prune_impl(X, M, K, b, bsr_keep_count((M / b) * (K / b), keep), dtype, out, ws, ws_bytes, stream);
+}
+
+bsr_status_t bsr_prune_k(const void *X, int64_t M, int64_t K, int32_t b, int64_t k, int32_t dtype, bsr_t *out,
+                         void *ws, size_t ws_bytes, void *stream) {
+    return prune_impl(X, M, K, b, k, dtype, out, ws, ws_bytes, stream);
+}
+
+bsr_status_t bsr_block_sumsq(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype, float *sumsq,
+                             void *stream) {
+    bsr_status_t st = check_shape(M, K, b, dtype);
+    if (st != BSR_OK) return st;
+    if (!X || !sumsq) return fail(BSR_ERR_INVALID_ARG, "X or sumsq is NULL");
+    if (!aligned16(X)) return fail(BSR_ERR_ALIGNMENT, "X is not 16-byte aligned");
+    return cuda_status(bsrp::launch_block_sumsq(X, M, K, b, elem_size(dtype), sumsq, static_cast<cudaStream_t>(stream)),
+                       "bsr_block_sumsq launch");
+}
+
+bsr_status_t bsr_decompress(const bsr_t *A, void *X_out, void *stream) {
+    bsr_status_t st = check_bsr(A);
+    if (st != BSR_OK) return st;
+    if (!X_out) return fail(BSR_ERR_INVALID_ARG, "X_out is NULL");
+    if (!aligned16(X_out)) return fail(BSR_ERR_ALIGNMENT, "X_out is not 16-byte aligned");
+    return cuda_status(bsrp::launch_decompress(A->rowptr, A->colidx, A->values, A->M, A->K, A->b,
+                                               elem_size(A->dtype), X_out, static_cast<cudaStream_t>(stream)),
+                       "bsr_decompress launch");
+}
+
+bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dW, int32_t accumulate,
+                       int32_t prec, void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_bsr(A);
+    if (st != BSR_OK) return st;
+    const int esy = elem_size(dy_dtype);
+    if (esy == 0) return fail(BSR_ERR_INVALID_ARG, "dy_dtype %d is not BSR_DT_F32 or BSR_DT_BF16", dy_dtype);
+    if (N <= 0 || N > (int64_t(1) << 30)) return fail(BSR_ERR_SHAPE, "N=%lld out of range", (long long)N);
+    if (!dY || !dW) return fail(BSR_ERR_INVALID_ARG, "dY or dW is NULL");
+    if (accumulate != 0 && accumulate != 1) return fail(BSR_ERR_INVALID_ARG, "accumulate must be 0 or 1");
+    if (!aligned16(dY) || !aligned16(dW)) return fail(BSR_ERR_ALIGNMENT, "dY or dW is not 16-byte aligned");
+    if ((N * esy) % 16 != 0 || (N * 4) % 16 != 0)
+        return fail(BSR_ERR_ALIGNMENT, "row pitch of dY/dW (N=%lld) is not a multiple of 16 bytes", (long long)N);
+    const int esx = elem_size(A->dtype);
+    if (overlap(dW, (size_t)A->K * N * 4, dY, (size_t)A->M * N * esy))
+        return fail(BSR_ERR_INVALID_ARG, "dW overlaps dY");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (prec) {
+        case BSR_PREC_FP32:
+            return cuda_status(bsrp::launch_wgrad_simt(A->rowptr, A->colidx, A->values, esx, A->M, A->K, A->b, dY,
+                                                       esy, N, dW, accumulate, s),
+                               "bsr_wgrad (fp32) launch");
+        case BSR_PREC_TF32:
+        case BSR_PREC_BF16: {
+            const int want = prec == BSR_PREC_TF32 ? BSR_DT_F32 : BSR_DT_BF16;
+            if (A->dtype != want || dy_dtype != want)
+                return fail(BSR_ERR_UNSUPPORTED, "%s tensor-core path needs %s values and dY",
+                            prec == BSR_PREC_TF32 ? "TF32" : "BF16", prec == BSR_PREC_TF32 ? "fp32" : "bf16");
+            if (A->b < 16) return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs b >= 16 (b=%d)", A->b);
+            if (N % 128 != 0) return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs N %% 128 == 0 (N=%lld)", (long long)N);
+            const size_t need = bsrp::wgrad_tc_ws_bytes(A->M, A->K, A->b, N);
+            if (need && (!ws || ws_bytes < need))
+                return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+            return cuda_status(bsrp::launch_wgrad_tc(A->rowptr, A->colidx, A->values, prec == BSR_PREC_TF32 ? 0 : 1,
+                                                     A->M, A->K, A->b, dY, N, dW, accumulate, ws, s),
+                               "bsr_wgrad (tensor-core) launch");
+        }
+        default:
+            return fail(BSR_ERR_INVALID_ARG, "prec %d is not a bsr_prec_t", prec);
+    }
+}
+
+const char *bsr_status_string(int32_t status) {
+    switch (status) {
+        case BSR_OK: return "BSR_OK";
+        case BSR_ERR_INVALID_ARG: return "BSR_ERR_INVALID_ARG";
+        case BSR_ERR_SHAPE: return "BSR_ERR_SHAPE";
+        case BSR_ERR_UNSUPPORTED: return "BSR_ERR_UNSUPPORTED";
+        case BSR_ERR_ALIGNMENT: return "BSR_ERR_ALIGNMENT";
+        case BSR_ERR_WORKSPACE: return "BSR_ERR_WORKSPACE";
+        case BSR_ERR_CUDA: return "BSR_ERR_CUDA";
+        default: return "BSR_ERR_UNKNOWN";
+    }
+}
+
+const char *bsr_last_error(void) { return g_last_error.c_str(); }
+
+const char *bsr_version(void) { return "bsrprune 0.1.0 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+// launch.h -- internal host-side launchers behind the C ABI (not exported).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace bsrp {
+
+// Workspace layout of bsr_prune (byte offsets; all 256-aligned).
+struct PruneWs {
+    size_t hdr, hist1, hist2, hist3, cta_cnt, sumsq, slot, total, zero_bytes;
+};
+constexpr int kMaxGrid = 2048;
+PruneWs prune_ws_layout(int64_t N);
+
+// Returns cudaSuccess or the launch error.
+cudaError_t launch_prune(const void *X, int64_t M, int64_t K, int b, int es, int64_t k,
+                         int32_t *rowptr, int32_t *colidx, void *values, void *ws,
+                         cudaStream_t stream);
+cudaError_t launch_block_sumsq(const void *X, int64_t M, int64_t K, int b, int es, float *sumsq,
+                               cudaStream_t stream);
+cudaError_t launch_decompress(const int32_t *rowptr, const int32_t *colidx, const void *values,
+                              int64_t M, int64_t K, int b, int es, void *Xout, cudaStream_t stream);
+
+// dW = X_bsr^T dY, fp32 SIMT path (deterministic).
+cudaError_t launch_wgrad_simt(const int32_t *rowptr, const int32_t *colidx, const void *values,
+                              int es_x, int64_t M, int64_t K, int b, const void *dY, int es_y,
+                              int64_t N, float *dW, int accumulate, cudaStream_t stream);
+
+// dW = X_bsr^T dY on tcgen05 tensor cores.  kind: 0 = tf32 (fp32 operands),
+// 1 = f16 (bf16 operands).
+size_t wgrad_tc_ws_bytes(int64_t M, int64_t K, int b, int64_t N);
+cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values,
+                            int kind, int64_t M, int64_t K, int b, const void *dY, int64_t N,
+                            float *dW, int accumulate, void *ws, cudaStream_t stream);
+
+}  // namespace bsrp

@@ -1,0 +1,541 @@
+// prune.cu -- block l2 prune/pack on sm_100a (rows a1-a4 of SURVEY §8a).
+//
+// One persistent, cooperatively launched kernel does the whole forward-side
+// step of the paper's operator:
+//
+//   phase 1  norms   : every warp streams one "unit" -- a 512-byte-wide strip
+//                      of b rows covering G = 512/(b*elem) consecutive blocks of
+//                      one block row -- with 128-bit loads, squares and sums
+//                      each element column sequentially over the b rows (one
+//                      fp32 accumulator per vector element), reduces the
+//                      lanes of a block with a fixed xor-shuffle tree, and
+//                      writes sumsq[f].  The first radix digit of the key is
+//                      counted in a shared-memory histogram.
+//   phase 2  select  : exact radix select of the k-th largest key over the
+//                      fp32 bit patterns (12 + 10 + 9 bits); every CTA derives
+//                      the same (prefix, shift, r) from the global histograms,
+//                      refining only while the boundary bin is split.  Keys
+//                      strictly above the prefix are kept, and the first r keys
+//                      equal to it in flat order (BJ tie rule).
+//   phase 3  scan    : per-CTA (above, tie) counts -> grid barrier -> CTA
+//                      prefix -> block-wide scans in flat order give every
+//                      kept block its output slot
+//                        pos(f) = above_before(f) + min(r, tie_before(f))
+//                      and rowptr / colidx.
+//   phase 4  pack    : the same warp units re-read only kept blocks (L2-hot
+//                      when X fits the 126 MB L2) and copy them as raw
+//                      integer vectors into values[pos][b][b].
+//
+// Units are statically partitioned into contiguous ranges per CTA, so phases
+// 1, 3 and 4 of a CTA touch the same flat range and need no cross-CTA data
+// except the histograms and the per-CTA counts.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace bsrp {
+
+constexpr int kThreads = 512;
+constexpr int kH1 = 4096, kH2 = 1024, kH3 = 512;  // digit sizes: key bits 30..19, 18..9, 8..0
+
+struct PruneParams {
+    const void *X;
+    int64_t K, nbr, nbc, N, k, units, upr;
+    int32_t *rowptr, *colidx;
+    void *values;
+    float *sumsq;
+    int32_t *slot;
+    uint32_t *bar, *hist1, *hist2, *hist3, *cta_cnt;
+};
+
+// Selection key of a block: fp32 bits of sumsq (>= 0, so the integer order is
+// the float order).  NaN is folded to 0x7fffffff and ranks above +inf (R12).
+__device__ __forceinline__ uint32_t key_of(float s) { return __float_as_uint(s) & 0x7fffffffu; }
+
+template <int ES, typename V>
+__device__ __forceinline__ float elem(const V &v, int e) {
+    if constexpr (ES == 4) {
+        return __uint_as_float(word(v, e));
+    } else {
+        uint32_t w = word(v, e >> 1);
+        return __uint_as_float((e & 1) ? (w & 0xffff0000u) : (w << 16));
+    }
+}
+
+template <int ES, int B>
+struct Geo {
+    static constexpr int VB = (B * ES >= 16) ? 16 : B * ES;  // bytes per lane vector
+    static constexpr int EPV = VB / ES;                      // elements per vector
+    static constexpr int LPB = B / EPV;                      // lanes per block row
+    static constexpr int G = kWarp / LPB;                    // blocks per warp unit
+    static constexpr int R = (B < 8) ? B : 8;                // rows in flight per lane
+    using V = typename Vec<VB>::T;
+};
+
+// Sum of squares of block (I, J) for this lane's vector column; returns the
+// block total on every lane of the block's lane segment.
+template <int ES, int B>
+__device__ __forceinline__ float block_sumsq_warp(const void *X, int64_t K, int64_t I, int64_t J, int sub,
+                                                  bool valid) {
+    // ld.global.cg (L2 only, normal L2 priority) so that the phase-4 re-read of
+    // the kept blocks hits L2 when X fits in it.
+    using G_ = Geo<ES, B>;
+    using V = typename G_::V;
+    float acc[G_::EPV];
+#pragma unroll
+    for (int e = 0; e < G_::EPV; ++e) acc[e] = 0.f;
+    if (valid) {
+        const int64_t rs = K / G_::EPV;  // row stride in vectors
+        const V *src = reinterpret_cast<const V *>(X) + (I * B) * rs + (J * B) / G_::EPV + sub;
+#pragma unroll
+        for (int r0 = 0; r0 < B; r0 += G_::R) {
+            V v[G_::R];
+#pragma unroll
+            for (int rr = 0; rr < G_::R; ++rr) v[rr] = __ldcg(src + (r0 + rr) * rs);
+#pragma unroll
+            for (int rr = 0; rr < G_::R; ++rr)
+#pragma unroll
+                for (int e = 0; e < G_::EPV; ++e) {
+                    float x = elem<ES>(v[rr], e);
+                    acc[e] = fmaf(x, x, acc[e]);
+                }
+        }
+    }
+    // pairwise tree over the vector's element columns
+#pragma unroll
+    for (int w = 1; w < G_::EPV; w <<= 1)
+#pragma unroll
+        for (int e = 0; e < G_::EPV; e += 2 * w) acc[e] = acc[e] + acc[e + w];
+    float s = acc[0];
+    // xor tree over the LPB lanes of the block (identical result on each lane)
+#pragma unroll
+    for (int off = 1; off < G_::LPB; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    return s;
+}
+
+// Exclusive block scan of 64-bit values (blockDim.x == kThreads).
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t *s_warp, uint64_t &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        uint64_t y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint64_t t = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            uint64_t y = __shfl_up_sync(0xffffffffu, t, off);
+            if (lane >= off) t += y;
+        }
+        s_warp[lane] = t;
+    }
+    __syncthreads();
+    const uint64_t base = wid > 0 ? s_warp[wid - 1] : 0;
+    total = s_warp[nw - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+// Find the bin that holds the `target`-th largest key (1-based) of a global
+// histogram with `nbins` bins; returns (bin, count strictly above the bin).
+// Thread 0 owns the top bins, so an exclusive prefix over threads = keys above.
+__device__ __forceinline__ void select_bin(const uint32_t *hist, int nbins, uint32_t target, uint64_t *s_warp,
+                                           uint32_t *s_out) {
+    const int per = nbins / kThreads;  // 8, 2 or 1
+    const int hi = nbins - threadIdx.x * per;
+    uint32_t h[8];
+    uint32_t local = 0;
+    for (int i = 0; i < per; ++i) {
+        h[i] = __ldcg(hist + hi - 1 - i);  // descending bins
+        local += h[i];
+    }
+    uint64_t total;
+    uint32_t run = (uint32_t)block_excl_scan(local, s_warp, total);
+    for (int i = 0; i < per; ++i) {
+        if (run < target && run + h[i] >= target) {
+            s_out[0] = hi - 1 - i;
+            s_out[1] = run;
+            s_out[2] = h[i];
+        }
+        run += h[i];
+    }
+    __syncthreads();
+}
+
+template <int ES, int B>
+__global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
+    using G_ = Geo<ES, B>;
+    using V = typename G_::V;
+    __shared__ uint32_t s_hist[kH1];
+    __shared__ uint64_t s_warp[32];
+    __shared__ uint32_t s_sel[4];
+
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kThreads / 32;
+    const int64_t u0 = (int64_t)blockIdx.x * p.units / gridDim.x;
+    const int64_t u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
+    auto flat_start = [&](int64_t u) -> int64_t {
+        return u >= p.units ? p.N : (u / p.upr) * p.nbc + (u % p.upr) * G_::G;
+    };
+    const int64_t f0 = flat_start(u0), f1 = flat_start(u1);
+    const int j = lane / G_::LPB, sub = lane % G_::LPB;
+    uint32_t nbar = 0;
+
+    // ---------------- phase 1: block sums of squares + level-1 histogram
+    for (int i = threadIdx.x; i < kH1; i += kThreads) s_hist[i] = 0;
+    __syncthreads();
+    for (int64_t u = u0 + wid; u < u1; u += nw) {
+        const int64_t I = u / p.upr, J = (u % p.upr) * G_::G + j;
+        const bool valid = J < p.nbc;
+        float s = block_sumsq_warp<ES, B>(p.X, p.K, I, J, sub, valid);
+        if (valid && sub == 0) {
+            p.sumsq[I * p.nbc + J] = s;
+            atomicAdd(&s_hist[key_of(s) >> 19], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kH1; i += kThreads)
+        if (s_hist[i]) atomicAdd(p.hist1 + i, s_hist[i]);
+    grid_barrier(p.bar, nbar++);
+
+    // ---------------- phase 2: radix select of the k-th largest key
+    const uint32_t k = (uint32_t)p.k;
+    select_bin(p.hist1, kH1, k, s_warp, s_sel);
+    uint32_t prefix = s_sel[0], above = s_sel[1], bincnt = s_sel[2];
+    int shift = 19;
+    uint32_t r = k - above;
+    if (r < bincnt) {  // boundary bin is split: refine on key bits 18..9
+        for (int i = threadIdx.x; i < kH2; i += kThreads) s_hist[i] = 0;
+        __syncthreads();
+        for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
+            uint32_t key = key_of(p.sumsq[f]);
+            if ((key >> 19) == prefix) atomicAdd(&s_hist[(key >> 9) & (kH2 - 1)], 1u);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kH2; i += kThreads)
+            if (s_hist[i]) atomicAdd(p.hist2 + i, s_hist[i]);
+        grid_barrier(p.bar, nbar++);
+        select_bin(p.hist2, kH2, r, s_warp, s_sel);
+        prefix = (prefix << 10) | s_sel[0];
+        above += s_sel[1];
+        bincnt = s_sel[2];
+        shift = 9;
+        r = k - above;
+        if (r < bincnt) {  // refine on key bits 8..0
+            for (int i = threadIdx.x; i < kH3; i += kThreads) s_hist[i] = 0;
+            __syncthreads();
+            for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
+                uint32_t key = key_of(p.sumsq[f]);
+                if ((key >> 9) == prefix) atomicAdd(&s_hist[key & (kH3 - 1)], 1u);
+            }
+            __syncthreads();
+            for (int i = threadIdx.x; i < kH3; i += kThreads)
+                if (s_hist[i]) atomicAdd(p.hist3 + i, s_hist[i]);
+            grid_barrier(p.bar, nbar++);
+            select_bin(p.hist3, kH3, r, s_warp, s_sel);
+            prefix = (prefix << 9) | s_sel[0];
+            above += s_sel[1];
+            shift = 0;
+            r = k - above;
+        }
+    }
+
+    // ---------------- phase 3: flat-order scan -> slots, colidx, rowptr
+    uint32_t na = 0, nt = 0;
+    for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
+        uint32_t kk = key_of(p.sumsq[f]) >> shift;
+        na += kk > prefix;
+        nt += kk == prefix;
+    }
+    {
+        uint64_t tot;
+        block_excl_scan(((uint64_t)na << 32) | nt, s_warp, tot);
+        if (threadIdx.x == 0) {
+            p.cta_cnt[2 * blockIdx.x] = (uint32_t)(tot >> 32);
+            p.cta_cnt[2 * blockIdx.x + 1] = (uint32_t)tot;
+        }
+    }
+    grid_barrier(p.bar, nbar++);
+    uint64_t pre = 0;
+    for (int c = threadIdx.x; c < (int)blockIdx.x; c += kThreads)
+        pre += ((uint64_t)__ldcg(p.cta_cnt + 2 * c) << 32) | __ldcg(p.cta_cnt + 2 * c + 1);
+    {
+        uint64_t tot;
+        block_excl_scan(pre, s_warp, tot);
+        pre = tot;
+    }
+    uint32_t base_a = (uint32_t)(pre >> 32), base_t = (uint32_t)pre;
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.rowptr[0] = 0;
+    for (int64_t fb = f0; fb < f1; fb += kThreads) {
+        const int64_t f = fb + threadIdx.x;
+        const bool in = f < f1;
+        uint32_t a = 0, t = 0;
+        if (in) {
+            uint32_t kk = key_of(p.sumsq[f]) >> shift;
+            a = kk > prefix;
+            t = kk == prefix;
+        }
+        uint64_t tot;
+        uint64_t ex = block_excl_scan(((uint64_t)a << 32) | t, s_warp, tot);
+        const uint32_t ab = base_a + (uint32_t)(ex >> 32), tb = base_t + (uint32_t)ex;
+        if (in) {
+            const bool kept = a || (t && tb < r);
+            const uint32_t pos = ab + min(r, tb);
+            const int64_t I = f / p.nbc, J = f - I * p.nbc;
+            p.slot[f] = kept ? (int32_t)pos : -1;
+            if (kept) p.colidx[pos] = (int32_t)J;
+            if (J == p.nbc - 1) p.rowptr[I + 1] = (int32_t)(ab + a + min(r, tb + t));
+        }
+        base_a += (uint32_t)(tot >> 32);
+        base_t += (uint32_t)tot;
+    }
+    __syncthreads();
+
+    // ---------------- phase 4: copy kept blocks (raw integer vectors)
+    for (int64_t u = u0 + wid; u < u1; u += nw) {
+        const int64_t I = u / p.upr, J = (u % p.upr) * G_::G + j;
+        const int32_t s = (J < p.nbc) ? p.slot[I * p.nbc + J] : -1;
+        if (s >= 0) {
+            const int64_t rs = p.K / G_::EPV;
+            const V *src = reinterpret_cast<const V *>(p.X) + (I * B) * rs + (J * B) / G_::EPV + sub;
+            V *dst = reinterpret_cast<V *>(p.values) + (int64_t)s * (B * B / G_::EPV) + sub;
+#pragma unroll
+            for (int r0 = 0; r0 < B; r0 += G_::R) {
+                V v[G_::R];
+#pragma unroll
+                for (int rr = 0; rr < G_::R; ++rr) v[rr] = __ldcg(src + (r0 + rr) * rs);
+#pragma unroll
+                for (int rr = 0; rr < G_::R; ++rr) __stcs(dst + (r0 + rr) * G_::LPB, v[rr]);
+            }
+        }
+    }
+}
+
+// k == N: every block kept, no norms needed -- a single copy pass.
+template <int ES, int B>
+__global__ void __launch_bounds__(256) keep_all_kernel(PruneParams p) {
+    using G_ = Geo<ES, B>;
+    using V = typename G_::V;
+    const int lane = threadIdx.x & 31;
+    const int j = lane / G_::LPB, sub = lane % G_::LPB;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t u = wg; u < p.units; u += nwg) {
+        const int64_t I = u / p.upr, J = (u % p.upr) * G_::G + j;
+        if (J >= p.nbc) continue;
+        const int64_t f = I * p.nbc + J;
+        if (sub == 0) {
+            p.colidx[f] = (int32_t)J;
+            if (J == 0) p.rowptr[I] = (int32_t)f;
+            if (I == p.nbr - 1 && J == p.nbc - 1) p.rowptr[p.nbr] = (int32_t)p.N;
+        }
+        const int64_t rs = p.K / G_::EPV;
+        const V *src = reinterpret_cast<const V *>(p.X) + (I * B) * rs + (J * B) / G_::EPV + sub;
+        V *dst = reinterpret_cast<V *>(p.values) + f * (B * B / G_::EPV) + sub;
+#pragma unroll
+        for (int r0 = 0; r0 < B; r0 += G_::R) {
+            V v[G_::R];
+#pragma unroll
+            for (int rr = 0; rr < G_::R; ++rr) v[rr] = ld_stream(src + (r0 + rr) * rs);
+#pragma unroll
+            for (int rr = 0; rr < G_::R; ++rr) __stcs(dst + (r0 + rr) * G_::LPB, v[rr]);
+        }
+    }
+}
+
+// Test hook: phase 1 only, written to a caller buffer.
+template <int ES, int B>
+__global__ void __launch_bounds__(256) sumsq_kernel(const void *X, int64_t K, int64_t nbc, int64_t units,
+                                                    int64_t upr, float *sumsq) {
+    using G_ = Geo<ES, B>;
+    const int lane = threadIdx.x & 31;
+    const int j = lane / G_::LPB, sub = lane % G_::LPB;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t u = wg; u < units; u += nwg) {
+        const int64_t I = u / upr, J = (u % upr) * G_::G + j;
+        const bool valid = J < nbc;
+        float s = block_sumsq_warp<ES, B>(X, K, I, J, sub, valid);
+        if (valid && sub == 0) sumsq[I * nbc + J] = s;
+    }
+}
+
+// BSR -> dense: every output row segment written once (zeros or the block).
+template <int ES, int B>
+__global__ void __launch_bounds__(256) decompress_kernel(const int32_t *__restrict__ rowptr,
+                                                         const int32_t *__restrict__ colidx,
+                                                         const void *__restrict__ values, int64_t K, int64_t nbc,
+                                                         int64_t units, int64_t upr, void *__restrict__ Xout) {
+    using G_ = Geo<ES, B>;
+    using V = typename G_::V;
+    const int lane = threadIdx.x & 31;
+    const int j = lane / G_::LPB, sub = lane % G_::LPB;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t u = wg; u < units; u += nwg) {
+        const int64_t I = u / upr, J = (u % upr) * G_::G + j;
+        if (J >= nbc) continue;
+        // binary search of J among the (ascending) stored columns of row I
+        int lo = __ldg(rowptr + I), hi = __ldg(rowptr + I + 1);
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (__ldg(colidx + mid) < J) lo = mid + 1; else hi = mid;
+        }
+        const bool present = lo < __ldg(rowptr + I + 1) && __ldg(colidx + lo) == J;
+        const int64_t rs = K / G_::EPV;
+        V *dst = reinterpret_cast<V *>(Xout) + (I * B) * rs + (J * B) / G_::EPV + sub;
+        if (present) {
+            const V *src = reinterpret_cast<const V *>(values) + (int64_t)lo * (B * B / G_::EPV) + sub;
+#pragma unroll
+            for (int r0 = 0; r0 < B; r0 += G_::R) {
+                V v[G_::R];
+#pragma unroll
+                for (int rr = 0; rr < G_::R; ++rr) v[rr] = ld_stream(src + (r0 + rr) * G_::LPB);
+#pragma unroll
+                for (int rr = 0; rr < G_::R; ++rr) __stcs(dst + (r0 + rr) * rs, v[rr]);
+            }
+        } else {
+            V z{};
+#pragma unroll 8
+            for (int r = 0; r < B; ++r) __stcs(dst + r * rs, z);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host side
+static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+PruneWs prune_ws_layout(int64_t N) {
+    PruneWs w;
+    size_t o = 0;
+    w.hdr = o;      o += align256(64 * 4);
+    w.hist1 = o;    o += align256(kH1 * 4);
+    w.hist2 = o;    o += align256(kH2 * 4);
+    w.hist3 = o;    o += align256(kH3 * 4);
+    w.zero_bytes = o;
+    w.cta_cnt = o;  o += align256(2 * kMaxGrid * 4);
+    w.sumsq = o;    o += align256((size_t)N * 4);
+    w.slot = o;     o += align256((size_t)N * 4);
+    w.total = o;
+    return w;
+}
+
+template <int ES, int B>
+static int units_per_row(int64_t nbc) {
+    return (int)((nbc + Geo<ES, B>::G - 1) / Geo<ES, B>::G);
+}
+
+static int num_sms() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+template <int ES, int B>
+static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, const PruneWs &w) {
+    if (p.k == 0) {
+        return cudaMemsetAsync(p.rowptr, 0, (size_t)(p.nbr + 1) * 4, stream);
+    }
+    if (p.k == p.N) {
+        int64_t blocks = std::min<int64_t>((p.units + 7) / 8, 148 * 16);
+        keep_all_kernel<ES, B><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, stream>>>(p);
+        return cudaGetLastError();
+    }
+    cudaError_t e = cudaMemsetAsync(ws, 0, w.zero_bytes, stream);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, prune_kernel<ES, B>, kThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorLaunchOutOfResources;
+    int64_t grid = (int64_t)occ * num_sms();
+    grid = std::min<int64_t>(grid, kMaxGrid);
+    grid = std::min<int64_t>(grid, std::max<int64_t>(1, (p.units + kThreads / 32 - 1) / (kThreads / 32)));
+    void *args[] = {&p};
+    return cudaLaunchCooperativeKernel((const void *)prune_kernel<ES, B>, dim3((unsigned)grid), dim3(kThreads),
+                                       args, 0, stream);
+}
+
+#define BSRP_DISPATCH_B(ES, b, CALL)     \
+    switch (b) {                         \
+        case 4: return CALL(ES, 4);      \
+        case 8: return CALL(ES, 8);      \
+        case 16: return CALL(ES, 16);    \
+        case 32: return CALL(ES, 32);    \
+        case 64: return CALL(ES, 64);    \
+        default: return cudaErrorInvalidValue; \
+    }
+
+cudaError_t launch_prune(const void *X, int64_t M, int64_t K, int b, int es, int64_t k, int32_t *rowptr,
+                         int32_t *colidx, void *values, void *ws, cudaStream_t stream) {
+    PruneParams p{};
+    p.X = X;
+    p.K = K;
+    p.nbr = M / b;
+    p.nbc = K / b;
+    p.N = p.nbr * p.nbc;
+    p.k = k;
+    p.rowptr = rowptr;
+    p.colidx = colidx;
+    p.values = values;
+    const PruneWs w = prune_ws_layout(p.N);
+    char *base = static_cast<char *>(ws);
+    p.bar = reinterpret_cast<uint32_t *>(base + w.hdr);
+    p.hist1 = reinterpret_cast<uint32_t *>(base + w.hist1);
+    p.hist2 = reinterpret_cast<uint32_t *>(base + w.hist2);
+    p.hist3 = reinterpret_cast<uint32_t *>(base + w.hist3);
+    p.cta_cnt = reinterpret_cast<uint32_t *>(base + w.cta_cnt);
+    p.sumsq = reinterpret_cast<float *>(base + w.sumsq);
+    p.slot = reinterpret_cast<int32_t *>(base + w.slot);
+#define CALL(ES_, B_) (p.upr = units_per_row<ES_, B_>(p.nbc), p.units = p.nbr * p.upr, \
+                       launch_prune_t<ES_, B_>(p, stream, ws, w))
+    if (es == 4) {
+        BSRP_DISPATCH_B(4, b, CALL)
+    } else {
+        BSRP_DISPATCH_B(2, b, CALL)
+    }
+#undef CALL
+}
+
+cudaError_t launch_block_sumsq(const void *X, int64_t M, int64_t K, int b, int es, float *sumsq,
+                               cudaStream_t stream) {
+    const int64_t nbr = M / b, nbc = K / b;
+#define CALL(ES_, B_) ([&]() {                                                              \
+        int64_t upr = units_per_row<ES_, B_>(nbc), units = nbr * upr;                     \
+        int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((units + 7) / 8, 148 * 16)); \
+        sumsq_kernel<ES_, B_><<<(unsigned)blocks, 256, 0, stream>>>(X, K, nbc, units, upr, sumsq); \
+        return cudaGetLastError();                                                        \
+    }())
+    if (es == 4) {
+        BSRP_DISPATCH_B(4, b, CALL)
+    } else {
+        BSRP_DISPATCH_B(2, b, CALL)
+    }
+#undef CALL
+}
+
+cudaError_t launch_decompress(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t M,
+                              int64_t K, int b, int es, void *Xout, cudaStream_t stream) {
+    const int64_t nbr = M / b, nbc = K / b;
+#define CALL(ES_, B_) ([&]() {                                                                   \
+        int64_t upr = units_per_row<ES_, B_>(nbc), units = nbr * upr;                          \
+        int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((units + 7) / 8, 148 * 16));      \
+        decompress_kernel<ES_, B_><<<(unsigned)blocks, 256, 0, stream>>>(rowptr, colidx, values, K, nbc, \
+                                                                         units, upr, Xout);    \
+        return cudaGetLastError();                                                             \
+    }())
+    if (es == 4) {
+        BSRP_DISPATCH_B(4, b, CALL)
+    } else {
+        BSRP_DISPATCH_B(2, b, CALL)
+    }
+#undef CALL
+}
+
+}  // namespace bsrp

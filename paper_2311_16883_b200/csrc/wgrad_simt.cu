@@ -1,0 +1,174 @@
+// wgrad_simt.cu -- the FP32 path of the BSR weight gradient (row a6).
+//
+//   dW[J*b + c][n] = sum over stored blocks (I, J), sum over r < b of
+//                    values(I,J)[r][c] * dY[I*b + r][n]          (BJ)
+//
+// fp32 FFMA with round-to-nearest in a FIXED order (ascending block row I,
+// then ascending r), so the result is deterministic and, per SURVEY A.4,
+// within ~2e-6..5e-6 relative Frobenius error of the fp64 oracle (the 1e-5
+// bar; plain TF32 cannot meet it).
+//
+// One CTA owns an output tile of b rows (block column J) x 128 columns of dY.
+// It finds the block rows that store (I, J) by a per-row binary search of
+// colidx (one thread per block row, compacted with a ballot so the order of I
+// is kept), and for each such block stages the b x b block and the b x 128
+// slab of dY in shared memory, then every thread accumulates its 4 x (b/8)
+// register tile.  Pruned blocks and block rows without a block in column J are
+// never read.
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace bsrp {
+
+constexpr int kSimtThreads = 256;
+constexpr int kNT = 128;  // dY columns per CTA
+
+template <int ES>
+__device__ __forceinline__ float4 load4(const void *base, int64_t idx) {  // 4 consecutive elements
+    if constexpr (ES == 4) {
+        return __ldg(reinterpret_cast<const float4 *>(static_cast<const float *>(base) + idx));
+    } else {
+        uint2 w = __ldg(reinterpret_cast<const uint2 *>(static_cast<const uint16_t *>(base) + idx));
+        return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u),
+                           __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xffff0000u));
+    }
+}
+
+template <int ESX, int ESY, int B>
+__global__ void __launch_bounds__(kSimtThreads) wgrad_simt_kernel(const int32_t *__restrict__ rowptr,
+                                                                   const int32_t *__restrict__ colidx,
+                                                                   const void *__restrict__ values,
+                                                                   const void *__restrict__ dY, int64_t nbr,
+                                                                   int64_t N, float *__restrict__ dW,
+                                                                   int accumulate) {
+    constexpr int CPT = (B >= 8) ? B / 8 : 1;  // output rows per thread
+    constexpr int RS = (B < 32) ? B : 32;       // block rows staged at a time
+    __shared__ __align__(16) float s_v[RS * B];
+    __shared__ __align__(16) float s_y[RS * kNT];
+    __shared__ int32_t s_pos[kSimtThreads];
+    __shared__ int32_t s_row[kSimtThreads];
+    __shared__ int32_t s_cnt[kSimtThreads / 32 + 1];
+
+    const int J = blockIdx.x;
+    const int64_t n0 = (int64_t)blockIdx.y * kNT;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const bool row_active = (B >= 8) || ty < B;
+
+    float acc[CPT][4];
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+
+    for (int64_t Ib = 0; Ib < nbr; Ib += kSimtThreads) {
+        // ---- block rows in [Ib, Ib+256) that store block column J, in order of I
+        const int64_t I = Ib + threadIdx.x;
+        int pos = -1;
+        if (I < nbr) {
+            int lo = __ldg(rowptr + I), hi = __ldg(rowptr + I + 1);
+            const int end = hi;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (__ldg(colidx + mid) < J) lo = mid + 1; else hi = mid;
+            }
+            if (lo < end && __ldg(colidx + lo) == J) pos = lo;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, pos >= 0);
+        if (tx == 0) s_cnt[ty] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int run = 0;
+            for (int w = 0; w < kSimtThreads / 32; ++w) { int c = s_cnt[w]; s_cnt[w] = run; run += c; }
+            s_cnt[kSimtThreads / 32] = run;
+        }
+        __syncthreads();
+        if (pos >= 0) {
+            const int slot = s_cnt[ty] + __popc(bal & ((1u << tx) - 1u));
+            s_pos[slot] = pos;
+            s_row[slot] = (int32_t)I;
+        }
+        __syncthreads();
+        const int cnt = s_cnt[kSimtThreads / 32];
+
+        for (int t = 0; t < cnt; ++t) {
+            const int64_t p = s_pos[t];
+            const int64_t Ir = s_row[t];
+            for (int r0 = 0; r0 < B; r0 += RS) {
+                // stage RS rows of the block and of the dY slab (b x 128)
+                for (int e = threadIdx.x * 4; e < RS * B; e += kSimtThreads * 4) {
+                    float4 v = load4<ESX>(values, p * B * B + (int64_t)r0 * B + e);
+                    *reinterpret_cast<float4 *>(s_v + e) = v;
+                }
+                for (int e = threadIdx.x * 4; e < RS * kNT; e += kSimtThreads * 4) {
+                    const int r = e / kNT, c = e % kNT;
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (n0 + c < N) v = load4<ESY>(dY, (Ir * B + r0 + r) * N + n0 + c);
+                    *reinterpret_cast<float4 *>(s_y + e) = v;
+                }
+                __syncthreads();
+                if (row_active) {
+#pragma unroll 4
+                    for (int r = 0; r < RS; ++r) {
+                        const float4 y = *reinterpret_cast<const float4 *>(s_y + r * kNT + 4 * tx);
+#pragma unroll
+                        for (int i = 0; i < CPT; ++i) {
+                            const float v = s_v[r * B + ty + 8 * i];
+                            acc[i][0] = fmaf(v, y.x, acc[i][0]);
+                            acc[i][1] = fmaf(v, y.y, acc[i][1]);
+                            acc[i][2] = fmaf(v, y.z, acc[i][2]);
+                            acc[i][3] = fmaf(v, y.w, acc[i][3]);
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    if (!row_active) return;
+    const int64_t n = n0 + 4 * tx;
+    if (n >= N) return;
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+        const int64_t row = (int64_t)J * B + ty + 8 * i;
+        float4 *out = reinterpret_cast<float4 *>(dW + row * N + n);
+        float4 o = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        if (accumulate) {
+            float4 old = *out;
+            o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+        }
+        *out = o;
+    }
+}
+
+template <int ESX, int ESY>
+static cudaError_t launch_simt_es(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t M,
+                                  int64_t K, int b, const void *dY, int64_t N, float *dW, int accumulate,
+                                  cudaStream_t stream) {
+    const int64_t nbr = M / b, nbc = K / b;
+    dim3 grid((unsigned)nbc, (unsigned)((N + kNT - 1) / kNT));
+    switch (b) {
+#define CASE(B_)                                                                                                \
+    case B_:                                                                                                    \
+        wgrad_simt_kernel<ESX, ESY, B_><<<grid, kSimtThreads, 0, stream>>>(rowptr, colidx, values, dY, nbr, N, \
+                                                                          dW, accumulate);                     \
+        return cudaGetLastError();
+        CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
+#undef CASE
+        default:
+            return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_wgrad_simt(const int32_t *rowptr, const int32_t *colidx, const void *values, int es_x,
+                              int64_t M, int64_t K, int b, const void *dY, int es_y, int64_t N, float *dW,
+                              int accumulate, cudaStream_t stream) {
+    if (es_x == 4 && es_y == 4)
+        return launch_simt_es<4, 4>(rowptr, colidx, values, M, K, b, dY, N, dW, accumulate, stream);
+    if (es_x == 4 && es_y == 2)
+        return launch_simt_es<4, 2>(rowptr, colidx, values, M, K, b, dY, N, dW, accumulate, stream);
+    if (es_x == 2 && es_y == 4)
+        return launch_simt_es<2, 4>(rowptr, colidx, values, M, K, b, dY, N, dW, accumulate, stream);
+    return launch_simt_es<2, 2>(rowptr, colidx, values, M, K, b, dY, N, dW, accumulate, stream);
+}
+
+}  // namespace bsrp
