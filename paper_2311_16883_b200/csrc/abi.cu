@@ -208,7 +208,7 @@ bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t
             const size_t need = bsrp::wgrad_tc_ws_bytes(A->M, A->K, A->b, N);
             if (need && (!ws || ws_bytes < need))
                 return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
-            return cuda_status(bsrp::launch_wgrad_tc(A->rowptr, A->colidx, A->values, prec == BSR_PREC_TF32 ? 0 : 1,
+            return cuda_status(bsrp::launch_wgrad_tc(A->rowptr, A->colidx, A->values, A->nnzb, prec == BSR_PREC_TF32 ? 0 : 1,
                                                      A->M, A->K, A->b, dY, N, dW, accumulate, ws, s),
                                "bsr_wgrad (tensor-core) launch");
         }

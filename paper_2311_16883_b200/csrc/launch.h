@@ -31,7 +31,7 @@ cudaError_t launch_wgrad_simt(const int32_t *rowptr, const int32_t *colidx, cons
 // 1 = f16 (bf16 operands).
 size_t wgrad_tc_ws_bytes(int64_t M, int64_t K, int b, int64_t N);
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values,
-                            int kind, int64_t M, int64_t K, int b, const void *dY, int64_t N,
-                            float *dW, int accumulate, void *ws, cudaStream_t stream);
+                            int64_t nnzb, int kind, int64_t M, int64_t K, int b, const void *dY,
+                            int64_t N, float *dW, int accumulate, void *ws, cudaStream_t stream);
 
 }  // namespace bsrp
