@@ -153,8 +153,9 @@ BSR_API bsr_status_t bsr_decompress(const bsr_t *A, void *X_out, void *stream);
  * `dy_dtype`.  accumulate = 0 overwrites dW, 1 adds to it.  Block rows and
  * blocks that were pruned contribute nothing and are never read.  `prec`
  * selects the arithmetic (see bsr_prec_t): FP32 accepts f32 or bf16 operands;
- * TF32 needs f32 values and f32 dY; BF16 needs bf16 values and bf16 dY, b in
- * {16, 32, 64} and N a multiple of 128 for the tensor-core paths. */
+ * TF32 needs f32 values and f32 dY and b in {32, 64}; BF16 needs bf16 values
+ * and bf16 dY and b in {16, 32, 64}; both tensor-core paths need N a multiple
+ * of 128.  Otherwise BSR_ERR_UNSUPPORTED. */
 BSR_API bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dW,
                        int32_t accumulate, int32_t prec, void *ws, size_t ws_bytes, void *stream);
 
@@ -163,6 +164,13 @@ BSR_API const char *bsr_status_string(int32_t status);
 
 /* Detail of the calling thread's last failing call ("" if none). */
 BSR_API const char *bsr_last_error(void);
+
+/* Number of CUDA kernels this library has launched in this process so far
+ * (all calls, all threads; memsets are not counted).  Diagnostic: lets a
+ * caller prove how many of the library's own kernels ran in a region.  Kernel
+ * launches replayed from a CUDA graph captured around a call are not counted
+ * again. */
+BSR_API uint64_t bsr_kernel_launches(void);
 
 /* Library version string, e.g. "bsrprune 0.1.0 sm_100a". */
 BSR_API const char *bsr_version(void);

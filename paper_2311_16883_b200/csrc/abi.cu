@@ -2,6 +2,7 @@
 // size queries, error reporting and dispatch to the sm_100a kernels.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -10,6 +11,11 @@
 
 #include "../../include/bsrprune.h"
 #include "launch.h"
+
+namespace bsrp {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace bsrp
 
 namespace {
 
@@ -204,6 +210,9 @@ bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t
                 return fail(BSR_ERR_UNSUPPORTED, "%s tensor-core path needs %s values and dY",
                             prec == BSR_PREC_TF32 ? "TF32" : "BF16", prec == BSR_PREC_TF32 ? "fp32" : "bf16");
             if (A->b < 16) return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs b >= 16 (b=%d)", A->b);
+            if (prec == BSR_PREC_TF32 && A->b < 32)
+                return fail(BSR_ERR_UNSUPPORTED, "TF32 tensor-core path needs b >= 32 (b=%d): MN-major tf32 operands "
+                            "need 128-byte block rows", A->b);
             if (N % 128 != 0) return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs N %% 128 == 0 (N=%lld)", (long long)N);
             const size_t need = bsrp::wgrad_tc_ws_bytes(A->M, A->K, A->b, N);
             if (need && (!ws || ws_bytes < need))
@@ -231,6 +240,8 @@ const char *bsr_status_string(int32_t status) {
 }
 
 const char *bsr_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t bsr_kernel_launches(void) { return bsrp::g_launches.load(std::memory_order_relaxed); }
 
 const char *bsr_version(void) { return "bsrprune 0.1.0 sm_100a"; }
 

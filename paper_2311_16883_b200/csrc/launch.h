@@ -6,6 +6,9 @@
 
 namespace bsrp {
 
+// Process-wide count of kernels this library has launched (bsr_kernel_launches).
+void count_launch(uint64_t n = 1);
+
 // Workspace layout of bsr_prune (byte offsets; all 256-aligned).
 struct PruneWs {
     size_t hdr, hist1, hist2, hist3, cta_cnt, sumsq, slot, total, zero_bytes;

@@ -446,6 +446,7 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
     if (p.k == p.N) {
         int64_t blocks = std::min<int64_t>((p.units + 7) / 8, 148 * 16);
         keep_all_kernel<ES, B><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, stream>>>(p);
+        count_launch();
         return cudaGetLastError();
     }
     cudaError_t e = cudaMemsetAsync(ws, 0, w.zero_bytes, stream);
@@ -458,6 +459,7 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
     grid = std::min<int64_t>(grid, kMaxGrid);
     grid = std::min<int64_t>(grid, std::max<int64_t>(1, (p.units + kThreads / 32 - 1) / (kThreads / 32)));
     void *args[] = {&p};
+    count_launch();
     return cudaLaunchCooperativeKernel((const void *)prune_kernel<ES, B>, dim3((unsigned)grid), dim3(kThreads),
                                        args, 0, stream);
 }
@@ -510,6 +512,7 @@ cudaError_t launch_block_sumsq(const void *X, int64_t M, int64_t K, int b, int e
         int64_t upr = units_per_row<ES_, B_>(nbc), units = nbr * upr;                     \
         int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((units + 7) / 8, 148 * 16)); \
         sumsq_kernel<ES_, B_><<<(unsigned)blocks, 256, 0, stream>>>(X, K, nbc, units, upr, sumsq); \
+        count_launch();                                                                   \
         return cudaGetLastError();                                                        \
     }())
     if (es == 4) {
@@ -528,6 +531,7 @@ cudaError_t launch_decompress(const int32_t *rowptr, const int32_t *colidx, cons
         int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((units + 7) / 8, 148 * 16));      \
         decompress_kernel<ES_, B_><<<(unsigned)blocks, 256, 0, stream>>>(rowptr, colidx, values, K, nbc, \
                                                                          units, upr, Xout);    \
+        count_launch();                                                                        \
         return cudaGetLastError();                                                             \
     }())
     if (es == 4) {

@@ -151,6 +151,7 @@ static cudaError_t launch_simt_es(const int32_t *rowptr, const int32_t *colidx, 
     case B_:                                                                                                    \
         wgrad_simt_kernel<ESX, ESY, B_><<<grid, kSimtThreads, 0, stream>>>(rowptr, colidx, values, dY, nbr, N, \
                                                                           dW, accumulate);                     \
+        count_launch();                                                                                         \
         return cudaGetLastError();
         CASE(4) CASE(8) CASE(16) CASE(32) CASE(64)
 #undef CASE

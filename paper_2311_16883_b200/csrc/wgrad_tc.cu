@@ -161,8 +161,19 @@ struct Cfg {
     static constexpr int B_ATOMS = B * ES / BW;
     static constexpr int BLOCK_BYTES = B * B * ES;
     static constexpr int B_LBO = B * BW;                    // bytes between N atoms
-    static constexpr int B_SBO = 8 * BW;                    // bytes between 8-row K groups
-    static constexpr uint32_t B_LAYOUT = BW == 128 ? 2u : BW == 64 ? 4u : 6u;  // SW128 / SW64 / SW32
+    // MN-major tf32 operands only exist in the 128-byte swizzle with 32-byte
+    // atomicity (UMMA layout type 1, TMA SWIZZLE_128B_ATOM_32B): 128-byte rows,
+    // 32-byte chunks permuted by (row % 4), K groups of 4 rows.  bf16 uses the
+    // plain SW32/64/128 layouts with K groups of 8 rows.
+    static constexpr bool TF32 = KIND == 0;
+    static constexpr int KGROUP = TF32 ? 4 : 8;             // K rows per swizzle group
+    static constexpr int A_SBO = KGROUP * 128;              // bytes between K groups of A
+    static constexpr uint32_t A_LAYOUT = TF32 ? 1u : 2u;
+    static constexpr int A_KSTEP = UK * 128;                // bytes per MMA K step in A
+    static constexpr int B_SBO = KGROUP * BW;               // bytes between K groups of B
+    static constexpr int B_KSTEP = UK * BW;                 // bytes per MMA K step in B
+    static constexpr uint32_t B_LAYOUT = TF32 ? 1u : BW == 128 ? 2u : BW == 64 ? 4u : 6u;  // SW128_32B / SW128 / SW64 / SW32
+    static_assert(!TF32 || BW == 128, "tf32 MN-major operands need 128-byte block rows (b >= 32)");
     static constexpr int MAX_RUN = 256 / B;                 // blocks per MMA (N <= 256)
 };
 
@@ -276,9 +287,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t idesc = instr_desc<KIND>((uint32_t)(L * B));
 #pragma unroll
                 for (int s = 0; s < B / C::UK; ++s) {
-                    const uint64_t ad = smem_desc(sA + s * (C::UK / 8) * 1024, C::A_LBO, 1024, 2u);
+                    const uint64_t ad = smem_desc(sA + s * C::A_KSTEP, C::A_LBO, C::A_SBO, C::A_LAYOUT);
                     const uint64_t bd =
-                        smem_desc(sB + q * C::BLOCK_BYTES + s * (C::UK / 8) * C::B_SBO, C::B_LBO, C::B_SBO, C::B_LAYOUT);
+                        smem_desc(sB + q * C::BLOCK_BYTES + s * C::B_KSTEP, C::B_LBO, C::B_SBO, C::B_LAYOUT);
                     tc_mma<KIND>(tmem + (uint32_t)(J * B), ad, bd, idesc, 1u);
                 }
                 q += L;
@@ -335,6 +346,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 static CUtensorMapSwizzle swz(int bytes) {
+    if (bytes == -128) return CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
     return bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
 }
 
@@ -390,9 +402,10 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     const Plan pl = plan_for<KIND, B>(M, K, N);
     const CUtensorMapDataType dt = KIND == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     CUtensorMap tm_dy, tm_val;
-    cudaError_t e = make_map(&tm_dy, dY, dt, C::ES, (uint64_t)N, (uint64_t)M, C::AW, B, 128);
+    cudaError_t e = make_map(&tm_dy, dY, dt, C::ES, (uint64_t)N, (uint64_t)M, C::AW, B, C::TF32 ? -128 : 128);
     if (e != cudaSuccess) return e;
-    e = make_map(&tm_val, values, dt, C::ES, (uint64_t)B, (uint64_t)nnzb * B, C::BW / C::ES, B, C::BW);
+    e = make_map(&tm_val, values, dt, C::ES, (uint64_t)B, (uint64_t)nnzb * B, C::BW / C::ES, B,
+                 C::TF32 ? -128 : C::BW);
     if (e != cudaSuccess) return e;
     Params p{};
     p.rowptr = rowptr;
@@ -421,6 +434,7 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((N / 128) * pl.nkr * pl.nsplit);
     kern<<<grid, kThreads, pl.smem, stream>>>(tm_dy, tm_val, p);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -436,7 +450,7 @@ cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const 
     }
 #define TC_CASE(KD, B_) \
     if (kind == KD && b == B_) return tc::launch_t<KD, B_>(rowptr, colidx, values, nnzb, M, K, dY, N, dW, accumulate, stream);
-    TC_CASE(0, 16) TC_CASE(0, 32) TC_CASE(0, 64) TC_CASE(1, 16) TC_CASE(1, 32) TC_CASE(1, 64)
+    TC_CASE(0, 32) TC_CASE(0, 64) TC_CASE(1, 16) TC_CASE(1, 32) TC_CASE(1, 64)
 #undef TC_CASE
     return cudaErrorInvalidValue;
 }
