@@ -214,9 +214,14 @@ bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t
                 return fail(BSR_ERR_UNSUPPORTED, "TF32 tensor-core path needs b >= 32 (b=%d): MN-major tf32 operands "
                             "need 128-byte block rows", A->b);
             if (N % 128 != 0) return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs N %% 128 == 0 (N=%lld)", (long long)N);
+            if (A->K / A->b > 65535)
+                return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs K/b < 65536 (K/b=%lld)", (long long)(A->K / A->b));
             const size_t need = bsrp::wgrad_tc_ws_bytes(A->M, A->K, A->b, N);
             if (need && (!ws || ws_bytes < need))
                 return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+            if (need && !aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
+            if (need && overlap(ws, need, dW, (size_t)A->K * N * 4))
+                return fail(BSR_ERR_INVALID_ARG, "workspace overlaps dW");
             return cuda_status(bsrp::launch_wgrad_tc(A->rowptr, A->colidx, A->values, A->nnzb, prec == BSR_PREC_TF32 ? 0 : 1,
                                                      A->M, A->K, A->b, dY, N, dW, accumulate, ws, s),
                                "bsr_wgrad (tensor-core) launch");

@@ -17,16 +17,23 @@
 // CTA's column range are never read.
 //
 // CTA = (128-column tile of dY) x (range of <= 512 kcols: TMEM columns) x
-// (range of block rows: split-K).  Warp roles: warp 0 = TMA producer (one
-// lane), warp 1 = MMA issuer (one lane), warp 2 = TMEM allocator, warps 4-7 =
-// epilogue (tcgen05.ld -> fp32 stores, or red.global.add across splits).
-// Shared-memory stages hold one block row each (A slab + its kept blocks),
-// swizzled by TMA exactly as the UMMA descriptors expect (SW128 for dY; SW32 /
-// SW64 / SW128 for blocks whose row is 32 / 64 / >=128 bytes wide).
+// (range of block rows: split-K).  Warp roles: warp 0 = TMA producer, warp 1 =
+// MMA issuer, warp 2 = TMEM allocator, warp 3 = block-row metadata prefetcher
+// (rowptr/colidx chunks into shared memory, double-buffered), warps 4-7 =
+// epilogue (tcgen05.ld -> fp32 stores of this split's partial tile).
+// Shared memory holds an A ring (one b x 128 dY slab per block row, loaded with
+// ONE 3-D TMA) and a B ring of block slots (a row's kept blocks are consecutive
+// in BSR storage and land in consecutive slots, loaded G blocks per 4-D TMA),
+// swizzled by TMA exactly as the UMMA descriptors expect.  The producer turns
+// each row into a list of MMA runs (consecutive block columns, N <= 256) so the
+// per-row instruction count of both single-thread roles stays small -- the
+// per-row issue cost, not HBM, bounds a naive version of this kernel.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -36,8 +43,19 @@ namespace bsrp {
 namespace tc {
 
 constexpr int kThreads = 256;
-constexpr int kMetaBytes = 64;     // per stage: [0] = block count (255 = end), [1..] = relative J
+// per A stage (uint2 units): [0].x = number of MMA runs (kEndMarker = no more rows),
+// [0].y = first B-ring slot; [1..] = one MMA run each: x = TMEM column | (slot
+// offset << 16), y = UMMA instruction descriptor (encodes N = run length * b)
+constexpr int kMetaPairs = 34;
+constexpr uint32_t kEndMarker = 0xFFFFu;
+constexpr int kStageExtra = kMetaPairs * 8 + 4 + 16;  // meta + slot-use word + full/empty mbarriers
 constexpr int kSmemBudget = 227 * 1024;
+constexpr int kColCap = 1024;      // kept blocks of one metadata chunk (colidx staged in smem; one run each at most)
+constexpr int kRowCap = 255;       // block rows of one metadata chunk
+// alignment slack + barriers/TMEM slot + rowptr/colidx scratch + two row-plan buffers
+// (16-byte row records + 8-byte run records)
+constexpr int kFixedSmem = 1024 + 1024 + 4 * (kRowCap + 1) + 2 * kColCap + 2 * (16 * kRowCap + 8 * kColCap);
+constexpr int kSplitSMs = 148;     // bound on split-K CTAs used to size the workspace (B200: 148 SMs)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -72,11 +90,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap *tm, uint64_t *bar, void *dst, int x, int y) {
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap *tm, uint64_t *bar, uint32_t dst, int x, int y, int z) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap *tm, uint64_t *bar, uint32_t dst, int x, int y, int z,
+                                            int w) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -142,10 +168,11 @@ __device__ __forceinline__ void tmem_st16_zero(uint32_t taddr) {
 
 struct Params {
     const int32_t *rowptr, *colidx;
-    float *dW;
+    float *dW, *ws;
     int64_t nbr, N, K;
     int nkr, nsplit, kr_blocks;  // kcol range = kr_blocks blocks
-    int stages, stage_bytes, mode;  // mode: 0 store, 1 load-add-store, 2 red.add
+    int stages, nbslots, mode;   // A-ring stages, B-ring block slots; mode: 0 store, 1 load-add-store, 3 partial -> ws[split]
+    int chunk_rows;              // block rows of one metadata chunk (rowptr + colidx staged in smem)
     uint32_t tmem_cols;
 };
 
@@ -175,31 +202,71 @@ struct Cfg {
     static constexpr uint32_t B_LAYOUT = TF32 ? 1u : BW == 128 ? 2u : BW == 64 ? 4u : 6u;  // SW128_32B / SW128 / SW64 / SW32
     static_assert(!TF32 || BW == 128, "tf32 MN-major operands need 128-byte block rows (b >= 32)");
     static constexpr int MAX_RUN = 256 / B;                 // blocks per MMA (N <= 256)
+    static constexpr int G = BLOCK_BYTES >= 8192 ? 1 : BLOCK_BYTES >= 4096 ? 2 : 4;  // blocks per B TMA
 };
+
+#ifdef WGRAD_TRACE
+__device__ unsigned long long g_trace[160][256];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TRACE(slot) (g_trace[blockIdx.x][(slot)] = gtime())
+#else
+#define TRACE(slot) ((void)0)
+#endif
+#ifndef WGRAD_TRACE_MODE
+#define WGRAD_TRACE_MODE 0  // dev experiments only: 1 = no loads, 2 = no MMAs
+#endif
+
+// Slow wait for warps that idle for the whole main loop (epilogue): back off so
+// they do not steal issue slots from the producer and MMA warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) __nanosleep(256);
+}
 
 template <int KIND, int B>
 __global__ void __launch_bounds__(kThreads, 1)
-    wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_val, Params p) {
+    wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_val,
+                    const __grid_constant__ CUtensorMap tm_dw, const __grid_constant__ CUtensorMap tm_ws, Params p) {
     using C = Cfg<KIND, B>;
+    // shared memory: [A ring: stages x A_BYTES][B ring: nbslots x BLOCK_BYTES][meta: stages x kMetaPairs]
+    //   [slot use: stages][mbarriers][TMEM slot][rowptr scratch][colidx scratch][2 x row records][2 x run records]
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *meta = smem + (size_t)p.stages * p.stage_bytes;
-    uint64_t *full = reinterpret_cast<uint64_t *>(meta + p.stages * kMetaBytes);
+    uint8_t *ringA = smem;
+    uint8_t *ringB = ringA + (size_t)p.stages * C::A_BYTES;
+    uint2 *meta = reinterpret_cast<uint2 *>(ringB + (size_t)p.nbslots * C::BLOCK_BYTES);
+    uint32_t *s_used = reinterpret_cast<uint32_t *>(meta + p.stages * kMetaPairs);
+    uint64_t *full = reinterpret_cast<uint64_t *>(s_used + ((p.stages + 1) & ~1));
     uint64_t *empty = full + p.stages;
     uint64_t *accfull = empty + p.stages;
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(accfull + 1);
+    uint64_t *plan_full = accfull + 1;     // [2]
+    uint64_t *plan_empty = plan_full + 2;  // [2]
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(plan_empty + 2);
+    int4 *s_rows = reinterpret_cast<int4 *>((reinterpret_cast<uintptr_t>(s_tmem + 4) + 15) & ~uintptr_t(15));
+    // s_rows [2][kRowCap]: cnt | nruns << 16, B-ring need, run offset, first value index
+    uint2 *s_runs = reinterpret_cast<uint2 *>(s_rows + 2 * kRowCap);      // [2][kColCap]
+    int32_t *s_rp = reinterpret_cast<int32_t *>(s_runs + 2 * kColCap);   // [kRowCap + 1]
+    uint16_t *s_col = reinterpret_cast<uint16_t *>(s_rp + kRowCap + 1);  // [kColCap]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // Consecutive CTAs take consecutive 128-column tiles of the same block rows,
+    // so CTAs that run together read adjacent 512-byte pieces of the same dY rows.
+    const int ntn = (int)(p.N / 128);
     int t = blockIdx.x;
-    const int split = t % p.nsplit;
-    t /= p.nsplit;
+    const int nt = t % ntn;
+    t /= ntn;
     const int kr = t % p.nkr;
-    const int nt = t / p.nkr;
+    const int split = t / p.nkr;
     const int n0 = nt * 128;
     const int nbc = (int)(p.K / B);
     const int J0 = kr * p.kr_blocks;
     const int nbJ = min(p.kr_blocks, nbc - J0);
     const int64_t Ib = (int64_t)split * p.nbr / p.nsplit, Ie = (int64_t)(split + 1) * p.nbr / p.nsplit;
+    const int nchunks = (int)((Ie - Ib + p.chunk_rows - 1) / p.chunk_rows);
+    if (threadIdx.x == 0) TRACE(0);
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_dy)) : "memory");
@@ -211,6 +278,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(empty + s, 1);
         }
         mbar_init(accfull, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(plan_full + i, 1);
+            mbar_init(plan_empty + i, 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -225,109 +296,261 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *s_tmem;
 
-    // zero the accumulator columns this CTA owns (MMAs then always accumulate)
-    if (warp >= 4) {
+    if (warp == 3) {
+        // ------------------------------------------------ row planner
+        // For each chunk of block rows: rowptr + colidx into shared memory, then
+        // one lane per row derives the row's kept-block count, B-ring need (G
+        // rounded), first value index and its MMA runs (consecutive block columns,
+        // <= MAX_RUN blocks, each a TMEM column + slot offset + instruction
+        // descriptor), written to a double-buffered plan one chunk ahead of the
+        // producer.  The single-thread producer and MMA roles then do almost no
+        // per-row arithmetic.
+        for (int c = 0; c < nchunks; ++c) {
+            const int buf = c & 1;
+            const int64_t Ic = Ib + (int64_t)c * p.chunk_rows;
+            const int nrow = (int)min((int64_t)p.chunk_rows, Ie - Ic);
+            for (int i = lane; i <= nrow; i += 32) s_rp[i] = __ldg(p.rowptr + Ic + i);
+            __syncwarp();
+            const int base = s_rp[0], total = s_rp[nrow] - base;
+            for (int e = lane; e < total; e += 32) s_col[e] = (uint16_t)__ldg(p.colidx + base + e);
+            if (lane == 0) mbar_wait(plan_empty + buf, ((c >> 1) & 1) ^ 1);
+            __syncwarp();
+            int4 *rows = s_rows + buf * kRowCap;
+            uint2 *runs = s_runs + buf * kColCap;
+            int run_base = 0;
+            for (int r0 = 0; r0 < nrow; r0 += 32) {
+                const int r = r0 + lane;
+                int q0 = 0, cnt = 0, nruns = 0;
+                if (r < nrow) {
+                    q0 = s_rp[r] - base;
+                    int q1 = s_rp[r + 1] - base;
+                    if (p.nkr > 1) {
+                        while (q0 < q1 && (int)s_col[q0] < J0) ++q0;
+                        int q = q0;
+                        while (q < q1 && (int)s_col[q] < J0 + nbJ) ++q;
+                        q1 = q;
+                    }
+                    cnt = q1 - q0;
+                    int jprev = -2, rlen = 0;
+                    for (int q = 0; q < cnt; ++q) {
+                        const int J = (int)s_col[q0 + q] - J0;
+                        if (J == jprev + 1 && rlen < C::MAX_RUN) {
+                            ++rlen;
+                        } else {
+                            ++nruns;
+                            rlen = 1;
+                        }
+                        jprev = J;
+                    }
+                }
+                // exclusive warp scan of nruns -> this row's run offset
+                int incl = nruns;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int off = run_base + incl - nruns;
+                run_base += __shfl_sync(0xffffffffu, incl, 31);
+                if (r < nrow) {
+                    int jprev = -2, rlen = 0, rstart = 0, k = off;
+                    for (int q = 0; q < cnt; ++q) {
+                        const int J = (int)s_col[q0 + q] - J0;
+                        if (J == jprev + 1 && rlen < C::MAX_RUN) {
+                            ++rlen;
+                        } else {
+                            if (rlen)
+                                runs[k++] = make_uint2((uint32_t)((jprev - rlen + 1) * B) | ((uint32_t)rstart << 16),
+                                                       instr_desc<KIND>((uint32_t)(rlen * B)));
+                            rstart = q;
+                            rlen = 1;
+                        }
+                        jprev = J;
+                    }
+                    if (rlen)
+                        runs[k++] = make_uint2((uint32_t)((jprev - rlen + 1) * B) | ((uint32_t)rstart << 16),
+                                               instr_desc<KIND>((uint32_t)(rlen * B)));
+                    rows[r] = make_int4(cnt | (nruns << 16), (cnt + C::G - 1) / C::G * C::G, off, base + q0);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(plan_full + buf);
+        }
+    } else if (warp >= 4) {
+        // zero the accumulator columns this CTA owns (MMAs then always accumulate)
         const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
         for (int c = 0; c < nbJ * B; c += 16) tmem_st16_zero(tmem + lane_base + c);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
+    if (warp == 1 || warp >= 4) {  // the MMA warp starts only after the accumulator is zeroed
+        tc_fence_before();
+        asm volatile("bar.sync 1, 160;" ::: "memory");
+        tc_fence_after();
+    }
 
     if (warp == 0 && lane == 0) {
-        // ------------------------------------------------ TMA producer
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int64_t I = Ib; I < Ie; ++I) {
-            const int p0 = __ldg(p.rowptr + I), p1 = __ldg(p.rowptr + I + 1);
-            int q0 = p0;
-            while (q0 < p1 && __ldg(p.colidx + q0) < J0) ++q0;
-            int q1 = q0;
-            while (q1 < p1 && __ldg(p.colidx + q1) < J0 + nbJ) ++q1;
-            const int cnt = q1 - q0;
-            if (cnt == 0) continue;
-            mbar_wait(empty + stage, phase ^ 1);
-            uint8_t *m = meta + stage * kMetaBytes;
-            m[0] = (uint8_t)cnt;
-            for (int q = 0; q < cnt; ++q) m[1 + q] = (uint8_t)(__ldg(p.colidx + q0 + q) - J0);
-            mbar_arrive_expect_tx(full + stage, (uint32_t)(C::A_BYTES + cnt * C::BLOCK_BYTES));
-            uint8_t *sA = smem + (size_t)stage * p.stage_bytes;
-            uint8_t *sB = sA + C::A_BYTES;
-#pragma unroll
-            for (int a = 0; a < C::A_ATOMS; ++a)
-                tma_load_2d(&tm_dy, full + stage, sA + a * C::A_LBO, n0 + a * C::AW, (int)(I * B));
-            for (int q = 0; q < cnt; ++q)
-#pragma unroll
-                for (int h = 0; h < C::B_ATOMS; ++h)
-                    tma_load_2d(&tm_val, full + stage, sB + q * C::BLOCK_BYTES + h * C::B_LBO, h * (C::BW / C::ES),
-                                (q0 + q) * B);
-            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        // ------------------------------------------------ TMA producer (one thread)
+        // Stage s of the A ring holds one block row's b x 128 dY slab (one 3-D TMA);
+        // its kept blocks take consecutive slots of the B ring (never wrapping: a
+        // row that would wrap starts at slot 0 and the tail slots are skipped),
+        // loaded G blocks per 4-D TMA.  Stages and slots are reclaimed in issue
+        // order as the MMA commits arrive.
+        int head = 0, tail = 0, in_flight = 0, bhead = 0, bfree = p.nbslots, nrows_tr = 0;
+        (void)nrows_tr;
+        uint32_t tail_ph = 0;
+        const uint32_t sA0 = smem_u32(ringA), sB0 = smem_u32(ringB);
+        TRACE(1);
+        for (int c = 0; c < nchunks; ++c) {
+            const int buf = c & 1;
+            const int64_t Ic = Ib + (int64_t)c * p.chunk_rows;
+            const int nrow = (int)min((int64_t)p.chunk_rows, Ie - Ic);
+            mbar_wait(plan_full + buf, (c >> 1) & 1);
+            if (c == 0) TRACE(205);
+            const int4 *rows = s_rows + buf * kRowCap;
+            const uint2 *runs = s_runs + buf * kColCap;
+            for (int r = 0; r < nrow; ++r) {
+                const int4 rr = rows[r];
+                const int cnt = rr.x & 0xFFFF;
+                if (cnt == 0) continue;
+                const int nruns = rr.x >> 16, need = rr.y;
+                const int waste = bhead + need > p.nbslots ? p.nbslots - bhead : 0;
+                while (in_flight == p.stages || bfree < need + waste) {  // reclaim the oldest stage
+                    mbar_wait(empty + tail, tail_ph);
+                    bfree += (int)s_used[tail];
+                    if (++tail == p.stages) { tail = 0; tail_ph ^= 1; }
+                    --in_flight;
+                }
+                const int slot0 = waste ? 0 : bhead;
+                uint2 *m = meta + head * kMetaPairs;
+                m[0] = make_uint2((uint32_t)nruns, (uint32_t)slot0);
+                for (int i = 0; i < nruns; ++i) m[1 + i] = runs[rr.z + i];
+                s_used[head] = (uint32_t)(need + waste);
+                if (WGRAD_TRACE_MODE & 1) {
+                    mbar_arrive(full + head);
+                } else {
+                    mbar_arrive_expect_tx(full + head, (uint32_t)(C::A_BYTES + need * C::BLOCK_BYTES));
+                    tma_load_3d(&tm_dy, full + head, sA0 + head * C::A_BYTES, 0, (int)(Ic + r) * B, n0 / C::AW);
+                    for (int g = 0; g < need; g += C::G)
+                        tma_load_4d(&tm_val, full + head, sB0 + (slot0 + g) * C::BLOCK_BYTES, 0, 0, 0, rr.w + g);
+                }
+                if (nrows_tr < 100) TRACE(2 + nrows_tr);
+                ++nrows_tr;
+                bhead = slot0 + need;
+                if (bhead == p.nbslots) bhead = 0;
+                bfree -= need + waste;
+                ++in_flight;
+                if (++head == p.stages) head = 0;
+            }
+            mbar_arrive(plan_empty + buf);
         }
-        mbar_wait(empty + stage, phase ^ 1);  // end marker
-        meta[stage * kMetaBytes] = 255;
-        mbar_arrive(full + stage);
+        while (in_flight == p.stages) {  // the end marker needs a free stage
+            mbar_wait(empty + tail, tail_ph);
+            if (++tail == p.stages) { tail = 0; tail_ph ^= 1; }
+            --in_flight;
+        }
+        meta[head * kMetaPairs] = make_uint2(kEndMarker, 0);
+        mbar_arrive(full + head);
     } else if (warp == 1 && lane == 0) {
-        // ------------------------------------------------ MMA issuer
-        int stage = 0;
+        // ------------------------------------------------ MMA issuer (one thread)
+        const uint64_t a_desc0 = smem_desc(smem_u32(ringA), C::A_LBO, C::A_SBO, C::A_LAYOUT);
+        const uint64_t b_desc0 = smem_desc(smem_u32(ringB), C::B_LBO, C::B_SBO, C::B_LAYOUT);
+        int stage = 0, nmma_tr = 0;
+        (void)nmma_tr;
         uint32_t phase = 0;
         for (;;) {
             mbar_wait(full + stage, phase);
             tc_fence_after();
-            const uint8_t *m = meta + stage * kMetaBytes;
-            const int cnt = m[0];
-            if (cnt == 255) break;
-            const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
-            const uint32_t sB = sA + C::A_BYTES;
-            int q = 0;
-            while (q < cnt) {
-                const int J = m[1 + q];
-                int L = 1;
-                while (q + L < cnt && L < C::MAX_RUN && m[1 + q + L] == J + L) ++L;
-                const uint32_t idesc = instr_desc<KIND>((uint32_t)(L * B));
+            if (nmma_tr < 100) TRACE(102 + nmma_tr);
+            ++nmma_tr;
+            const uint2 *m = meta + stage * kMetaPairs;
+            const uint2 m0 = m[0];
+            if (m0.x == kEndMarker) break;
+            const uint64_t a_desc = a_desc0 + (uint64_t)((stage * C::A_BYTES) >> 4);
+            const uint64_t b_base = b_desc0 + (uint64_t)((m0.y * C::BLOCK_BYTES) >> 4);
+            for (uint32_t i = 0; i < m0.x; ++i) {
+                const uint2 run = m[1 + i];
+                const uint64_t b_desc = b_base + (uint64_t)(((run.x >> 16) * C::BLOCK_BYTES) >> 4);
+                const uint32_t d = tmem + (run.x & 0xFFFFu);
 #pragma unroll
-                for (int s = 0; s < B / C::UK; ++s) {
-                    const uint64_t ad = smem_desc(sA + s * C::A_KSTEP, C::A_LBO, C::A_SBO, C::A_LAYOUT);
-                    const uint64_t bd =
-                        smem_desc(sB + q * C::BLOCK_BYTES + s * C::B_KSTEP, C::B_LBO, C::B_SBO, C::B_LAYOUT);
-                    tc_mma<KIND>(tmem + (uint32_t)(J * B), ad, bd, idesc, 1u);
-                }
-                q += L;
+                for (int s = 0; s < B / C::UK; ++s)
+                    if (!(WGRAD_TRACE_MODE & 2)) tc_mma<KIND>(d, a_desc + (uint64_t)((s * C::A_KSTEP) >> 4), b_desc + (uint64_t)((s * C::B_KSTEP) >> 4),
+                                 run.y, 1u);
             }
-            tc_commit(empty + stage);  // frees the stage once these MMAs complete
+            tc_commit(empty + stage);  // frees the stage (and its B slots) once these MMAs complete
             if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
         tc_commit(accfull);
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
-        mbar_wait(accfull, 0);
+        // TMEM -> registers -> a [32 kcol][128 n] fp32 staging tile in the (now
+        // idle) A ring -> one TMA bulk tensor store (or reduce-add) per 16 kcols.
+        // Full 512-byte row segments leave the SM through the TMA unit instead of
+        // 128-byte scattered STGs.  mode 3 stores this split's partial tile into
+        // its own workspace slice (summed afterwards in split order:
+        // deterministic); mode 1 adds into dW (accumulate, one split).
+        mbar_wait_sleep(accfull, 0);
         tc_fence_after();
+        if (threadIdx.x == 128) TRACE(203);
         const int ew = warp - 4;
-        const int64_t n = n0 + ew * 32 + lane;
         const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
-        for (int c = 0; c < nbJ * B; c += 16) {
-            uint32_t v[16];
+        float *stage_buf = reinterpret_cast<float *>(ringA);  // 2 x [32][128]
+        const int ncols = nbJ * B;
+        const int row0 = (p.mode == 3 ? split * (int)p.K : 0) + J0 * B;
+        const CUtensorMap *tm_o = p.mode == 3 ? &tm_ws : &tm_dw;
+        for (int c = 0, it = 0; c < ncols; c += 32, ++it) {
+            float *sb = stage_buf + (it & 1) * (32 * 128);
+            if (it >= 2) {  // the TMA store issued two chunks ago must have finished reading this buffer
+                if (threadIdx.x == 128) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+            }
+            uint32_t v[32];
             TMEM_LD16(tmem + lane_base + c, v);
+            TMEM_LD16(tmem + lane_base + c + 16, (v + 16));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                float *dst = p.dW + ((int64_t)J0 * B + c + i) * p.N + n;
-                const float x = __uint_as_float(v[i]);
-                if (p.mode == 2) {
-                    atomicAdd(dst, x);
-                } else if (p.mode == 1) {
-                    *dst += x;
-                } else {
-                    *dst = x;
+            for (int i = 0; i < 32; ++i) sb[i * 128 + ew * 32 + lane] = __uint_as_float(v[i]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("bar.sync 2, 128;" ::: "memory");
+            if (threadIdx.x == 128) {
+                const int nh = min(32, ncols - c) / 16;
+                for (int h = 0; h < nh; ++h) {
+                    const uint32_t src = smem_u32(sb + h * 16 * 128);
+                    if (p.mode == 1)
+                        asm volatile(
+                            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                reinterpret_cast<uint64_t>(tm_o)),
+                            "r"(n0), "r"(row0 + c + h * 16), "r"(src)
+                            : "memory");
+                    else
+                        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                         reinterpret_cast<uint64_t>(tm_o)),
+                                     "r"(n0), "r"(row0 + c + h * 16), "r"(src)
+                                     : "memory");
                 }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
         }
+        if (threadIdx.x == 128) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
+    if (threadIdx.x == 128) TRACE(204);
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
+    }
+}
+
+// dW (+)= sum over splits of the partial tiles, in split order (deterministic).
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4 *__restrict__ ws, float4 *__restrict__ dW,
+                                                            int64_t n4, int nsplit, int accumulate) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 a = accumulate ? dW[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s = 0; s < nsplit; ++s) {
+            const float4 v = __ldcs(ws + (size_t)s * n4 + i);
+            a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+        }
+        dW[i] = a;
     }
 }
 
@@ -346,67 +569,110 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 static CUtensorMapSwizzle swz(int bytes) {
+    if (bytes == 0) return CU_TENSOR_MAP_SWIZZLE_NONE;
     if (bytes == -128) return CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
     return bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
 }
 
-static cudaError_t make_map(CUtensorMap *tm, const void *base, CUtensorMapDataType dt, int es, uint64_t cols,
-                            uint64_t rows, uint32_t box_cols, uint32_t box_rows, int swizzle_bytes) {
+// Tensor map with explicit dims / byte strides / box (dims[0] contiguous).
+static cudaError_t make_map(CUtensorMap *tm, const void *base, CUtensorMapDataType dt, int rank, const cuuint64_t *dims,
+                            const cuuint64_t *strides, const cuuint32_t *box, int swizzle_bytes) {
     auto fn = encode_fn();
     if (!fn) return cudaErrorNotSupported;
-    cuuint64_t dims[2] = {cols, rows};
-    cuuint64_t strides[1] = {cols * (cuuint64_t)es};
-    cuuint32_t box[2] = {box_cols, box_rows};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(tm, dt, 2, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = fn(tm, dt, rank, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     swz(swizzle_bytes), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 struct Plan {
-    int kr_blocks, nkr, stages, stage_bytes, nsplit, smem;
+    int kr_blocks, nkr, stages, nbslots, nsplit, smem, chunk_rows;
     uint32_t tmem_cols;
 };
 
+// sms: SMs the split-K grid may fill (the device's count at launch, kSplitSMs
+// for the pure workspace query).  avg_cnt: expected kept blocks per block row
+// inside one TMEM column range (sizes the A ring against the B ring).
 template <int KIND, int B>
-static Plan plan_for(int64_t M, int64_t K, int64_t N) {
+static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms, double avg_cnt = -1.0) {
     using C = Cfg<KIND, B>;
     Plan pl{};
     const int nbc = (int)(K / B);
-    const int fixed = 1024 + 256;  // alignment slack + barriers + TMEM slot
-    // largest kcol range (<= 512 TMEM columns) that still leaves >= 3 stages
+    const int ring = kSmemBudget - kFixedSmem;
+    // largest kcol range (<= 512 TMEM columns) whose full row (A slab + every
+    // block) fits twice in the rings
     int maxb = std::min(512 / B, nbc);
-    while (maxb > 1 && 3 * (C::A_BYTES + maxb * C::BLOCK_BYTES + kMetaBytes) + fixed > kSmemBudget) --maxb;
+    auto need_of = [](int blocks) { return (blocks + C::G - 1) / C::G * C::G; };
+    while (maxb > 1 && 2 * (C::A_BYTES + kStageExtra) + 2 * need_of(maxb) * C::BLOCK_BYTES > ring) --maxb;
     pl.nkr = (nbc + maxb - 1) / maxb;
     pl.kr_blocks = (nbc + pl.nkr - 1) / pl.nkr;
-    pl.stage_bytes = (C::A_BYTES + pl.kr_blocks * C::BLOCK_BYTES + 1023) & ~1023;
-    pl.stages = std::min(8, (kSmemBudget - fixed) / (pl.stage_bytes + kMetaBytes));
-    pl.smem = pl.stages * (pl.stage_bytes + kMetaBytes) + fixed;
+    if (avg_cnt < 0) avg_cnt = pl.kr_blocks;
+    avg_cnt = std::max(1.0, std::min<double>(avg_cnt, pl.kr_blocks));
+    // rows in flight: stages x (A slab + avg_cnt blocks) fills the ring
+    // rows in flight: stages x (A slab + the average row's block slots) fills the ring
+    const double avg_need = std::ceil(avg_cnt / C::G) * C::G + 0.5 * (C::G - 1);
+    int stages = (int)(ring / (C::A_BYTES + kStageExtra + avg_need * C::BLOCK_BYTES));
+    stages = std::max(2, std::min(64, stages));
+    int nb = (ring - stages * (C::A_BYTES + kStageExtra)) / C::BLOCK_BYTES;
+    while (nb < 2 * need_of(pl.kr_blocks) && stages > 2) {  // a full row must fit even after a wrap
+        --stages;
+        nb = (ring - stages * (C::A_BYTES + kStageExtra)) / C::BLOCK_BYTES;
+    }
+    pl.stages = stages;
+    pl.nbslots = nb;
+    pl.smem = stages * (C::A_BYTES + kStageExtra) + pl.nbslots * C::BLOCK_BYTES + kFixedSmem;
+    pl.chunk_rows = std::max(1, std::min(kRowCap, kColCap / nbc));  // a chunk's kept blocks fit the colidx/run buffers
     uint32_t cols = 32;
     while (cols < (uint32_t)(pl.kr_blocks * B)) cols <<= 1;
     pl.tmem_cols = cols;
     const int64_t tiles = (N / 128) * pl.nkr;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t nbr = M / B;
-    pl.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nbr, sms / std::max<int64_t>(1, tiles)));
+    const int64_t cap = std::min<int64_t>(sms, kSplitSMs);
+    pl.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nbr, cap / std::max<int64_t>(1, tiles)));
     return pl;
 }
 
 template <int KIND, int B>
 static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
                             int64_t M, int64_t K, const void *dY, int64_t N, float *dW, int accumulate,
-                            cudaStream_t stream) {
+                            float *ws, cudaStream_t stream) {
     using C = Cfg<KIND, B>;
-    const Plan pl = plan_for<KIND, B>(M, K, N);
+    int dev = 0, sms = kSplitSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // kept blocks per block row inside one TMEM column range, on average
+    Plan pl = plan_for<KIND, B>(M, K, N, sms);
+    const double avg_cnt = (double)nnzb / (double)(M / B) * pl.kr_blocks / (double)(K / B);
+    pl = plan_for<KIND, B>(M, K, N, sms, avg_cnt);
     const CUtensorMapDataType dt = KIND == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     CUtensorMap tm_dy, tm_val;
-    cudaError_t e = make_map(&tm_dy, dY, dt, C::ES, (uint64_t)N, (uint64_t)M, C::AW, B, C::TF32 ? -128 : 128);
+    // dY as (column within a 128-byte atom, row, atom): one box = the b x 128 slab
+    // of a block row, atom-major in shared memory (A_LBO apart)
+    const cuuint64_t dy_dims[3] = {(cuuint64_t)C::AW, (cuuint64_t)M, (cuuint64_t)(N / C::AW)};
+    const cuuint64_t dy_str[2] = {(cuuint64_t)N * C::ES, 128};
+    const cuuint32_t dy_box[3] = {(cuuint32_t)C::AW, (cuuint32_t)B, (cuuint32_t)C::A_ATOMS};
+    cudaError_t e = make_map(&tm_dy, dY, dt, 3, dy_dims, dy_str, dy_box, C::TF32 ? -128 : 128);
     if (e != cudaSuccess) return e;
-    e = make_map(&tm_val, values, dt, C::ES, (uint64_t)B, (uint64_t)nnzb * B, C::BW / C::ES, B,
-                 C::TF32 ? -128 : C::BW);
+    // values as (element within a swizzle atom row, block row, atom, block): one
+    // box = G consecutive stored blocks, each atom-major (B_LBO apart)
+    const cuuint64_t v_dims[4] = {(cuuint64_t)(C::BW / C::ES), (cuuint64_t)B, (cuuint64_t)C::B_ATOMS, (cuuint64_t)nnzb};
+    const cuuint64_t v_str[3] = {(cuuint64_t)B * C::ES, (cuuint64_t)C::BW, (cuuint64_t)C::BLOCK_BYTES};
+    const cuuint32_t v_box[4] = {(cuuint32_t)(C::BW / C::ES), (cuuint32_t)B, (cuuint32_t)C::B_ATOMS, (cuuint32_t)C::G};
+    e = make_map(&tm_val, values, dt, 4, v_dims, v_str, v_box, C::TF32 ? -128 : C::BW);
     if (e != cudaSuccess) return e;
+    // epilogue outputs: dW (K x N fp32) and the split-K workspace (nsplit*K x N), 128 x 16 boxes
+    CUtensorMap tm_dw, tm_ws;
+    const cuuint64_t o_dims[2] = {(cuuint64_t)N, (cuuint64_t)K};
+    const cuuint64_t o_str[1] = {(cuuint64_t)N * 4};
+    const cuuint32_t o_box[2] = {128, 16};
+    e = make_map(&tm_dw, dW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, o_dims, o_str, o_box, 0);
+    if (e != cudaSuccess) return e;
+    tm_ws = tm_dw;
+    if (pl.nsplit > 1) {
+        const cuuint64_t w_dims[2] = {(cuuint64_t)N, (cuuint64_t)K * pl.nsplit};
+        e = make_map(&tm_ws, ws, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, w_dims, o_str, o_box, 0);
+        if (e != cudaSuccess) return e;
+    }
     Params p{};
     p.rowptr = rowptr;
     p.colidx = colidx;
@@ -418,38 +684,52 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     p.nsplit = pl.nsplit;
     p.kr_blocks = pl.kr_blocks;
     p.stages = pl.stages;
-    p.stage_bytes = pl.stage_bytes;
+    p.nbslots = pl.nbslots;
     p.tmem_cols = pl.tmem_cols;
-    if (pl.nsplit > 1) {
-        p.mode = 2;
-        if (!accumulate) {
-            e = cudaMemsetAsync(dW, 0, (size_t)K * N * sizeof(float), stream);
-            if (e != cudaSuccess) return e;
-        }
-    } else {
-        p.mode = accumulate ? 1 : 0;
-    }
+    p.chunk_rows = pl.chunk_rows;
+    p.ws = ws;
+    p.mode = pl.nsplit > 1 ? 3 : accumulate ? 1 : 0;
     auto kern = wgrad_tc_kernel<KIND, B>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((N / 128) * pl.nkr * pl.nsplit);
-    kern<<<grid, kThreads, pl.smem, stream>>>(tm_dy, tm_val, p);
+    kern<<<grid, kThreads, pl.smem, stream>>>(tm_dy, tm_val, tm_dw, tm_ws, p);
+    count_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess || pl.nsplit == 1) return e;
+    const int64_t n4 = K * N / 4;
+    const unsigned rgrid = (unsigned)std::min<int64_t>((n4 + 255) / 256, sms * 8);
+    splitk_reduce_kernel<<<rgrid, 256, 0, stream>>>(reinterpret_cast<const float4 *>(ws),
+                                                    reinterpret_cast<float4 *>(dW), n4, pl.nsplit, accumulate);
     count_launch();
     return cudaGetLastError();
 }
 
 }  // namespace tc
 
-size_t wgrad_tc_ws_bytes(int64_t, int64_t, int, int64_t) { return 0; }
+size_t wgrad_tc_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
+    tc::Plan pl{};
+#define WS_CASE(B_) if (b == B_) pl = tc::plan_for<1, B_>(M, K, N, tc::kSplitSMs);
+    WS_CASE(16) WS_CASE(32) WS_CASE(64)
+#undef WS_CASE
+    // the tf32 plan has fewer TMEM-column ranges than or as many as the bf16 one,
+    // hence at least as many splits: take the larger of the two
+    tc::Plan pt{};
+    if (b == 32) pt = tc::plan_for<0, 32>(M, K, N, tc::kSplitSMs);
+    if (b == 64) pt = tc::plan_for<0, 64>(M, K, N, tc::kSplitSMs);
+    const int ns = std::max(pl.nsplit, pt.nsplit);
+    return ns > 1 ? (size_t)ns * K * N * sizeof(float) : 0;
+}
 
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
                             int kind, int64_t M, int64_t K, int b, const void *dY, int64_t N, float *dW,
-                            int accumulate, void *, cudaStream_t stream) {
+                            int accumulate, void *ws, cudaStream_t stream) {
     if (!values || nnzb == 0) {  // no stored block: dW = 0 (or unchanged)
         return accumulate ? cudaSuccess : cudaMemsetAsync(dW, 0, (size_t)K * N * sizeof(float), stream);
     }
 #define TC_CASE(KD, B_) \
-    if (kind == KD && b == B_) return tc::launch_t<KD, B_>(rowptr, colidx, values, nnzb, M, K, dY, N, dW, accumulate, stream);
+    if (kind == KD && b == B_) return tc::launch_t<KD, B_>(rowptr, colidx, values, nnzb, M, K, dY, N, dW, accumulate, \
+                                                            static_cast<float *>(ws), stream);
     TC_CASE(0, 32) TC_CASE(0, 64) TC_CASE(1, 16) TC_CASE(1, 32) TC_CASE(1, 64)
 #undef TC_CASE
     return cudaErrorInvalidValue;

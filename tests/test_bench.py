@@ -32,6 +32,8 @@ def test_native_arm_gpu():
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
                 "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "e2e", "gpu_launches"):
         assert key in d, key
-    assert d["gpu_launches"] == 3 * 20
+    per_step = d["gpu_launches_per_step"]
+    assert set(per_step) == {"prune", "wgrad", "decompress"} and min(per_step.values()) >= 1
+    assert d["gpu_launches"] == sum(per_step.values()) * 20
     assert 0 < d["roofline"]["frac"] < 1.5
     assert d["e2e"]["h2d_bytes_per_step"] == 25088 * 384 * 4 + 25088 * 1536 * 4
