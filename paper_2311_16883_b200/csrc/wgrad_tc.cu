@@ -43,12 +43,13 @@ namespace bsrp {
 namespace tc {
 
 constexpr int kThreads = 256;
-// per A stage (uint2 units): [0].x = number of MMA runs (kEndMarker = no more rows),
-// [0].y = first B-ring slot; [1..] = one MMA run each: x = TMEM column | (slot
-// offset << 16), y = UMMA instruction descriptor (encodes N = run length * b)
-constexpr int kMetaPairs = 34;
+// per stage (uint4 units), written by the B producer: [0].x = number of MMA runs
+// (kEndMarker = no more rows); [1..] = one MMA run each, ready to issue:
+// x = TMEM address of its first column, y = low word of the B descriptor (k-step
+// 0), z = UMMA instruction descriptor (encodes N = run length * b)
+constexpr int kMetaQuads = 34;
 constexpr uint32_t kEndMarker = 0xFFFFu;
-constexpr int kStageExtra = kMetaPairs * 8 + 4 + 16;  // meta + slot-use word + full/empty mbarriers
+constexpr int kStageExtra = kMetaQuads * 16 + 4 + 16;  // meta + slot-use word + full/empty mbarriers
 constexpr int kSmemBudget = 227 * 1024;
 constexpr int kColCap = 1024;      // kept blocks of one metadata chunk (colidx staged in smem; one run each at most)
 constexpr int kRowCap = 255;       // block rows of one metadata chunk
@@ -130,6 +131,65 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_
     }
 }
 
+// All B/UK k-steps of one MMA run in a single asm block: descriptors advance by
+// constant byte offsets (>> 4) inside PTX, so the issuing thread moves the base
+// descriptors into uniform registers once per run instead of once per MMA.
+#define BSRP_MMA2(KS)                                                                                    \
+    asm volatile("{\n.reg .b64 a1, b1;\n"                                                                 \
+                 "add.s64 a1, %1, %4;\nadd.s64 b1, %2, %5;\n"                                             \
+                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], %1, %2, %3, 1;\n"                          \
+                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], a1, b1, %3, 1;\n}\n" ::"r"(d_tmem),         \
+                 "l"(a_desc), "l"(b_desc), "r"(idesc), "n"(AK), "n"(BK))
+#define BSRP_MMA4(KS)                                                                                    \
+    asm volatile("{\n.reg .b64 a1, b1, a2, b2, a3, b3;\n"                                                 \
+                 "add.s64 a1, %1, %4;\nadd.s64 b1, %2, %5;\n"                                             \
+                 "add.s64 a2, %1, %6;\nadd.s64 b2, %2, %7;\n"                                             \
+                 "add.s64 a3, %1, %8;\nadd.s64 b3, %2, %9;\n"                                             \
+                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], %1, %2, %3, 1;\n"                          \
+                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], a1, b1, %3, 1;\n"                          \
+                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], a2, b2, %3, 1;\n"                          \
+                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], a3, b3, %3, 1;\n}\n" ::"r"(d_tmem),         \
+                 "l"(a_desc), "l"(b_desc), "r"(idesc), "n"(AK), "n"(BK), "n"(2 * AK), "n"(2 * BK),         \
+                 "n"(3 * AK), "n"(3 * BK))
+template <int KIND, int NSTEP, int AK, int BK>
+__device__ __forceinline__ void tc_mma_run(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc) {
+    if constexpr (NSTEP == 1) {
+        tc_mma<KIND>(d_tmem, a_desc, b_desc, idesc, 1u);
+    } else if constexpr (NSTEP == 2) {
+        if constexpr (KIND == 1) BSRP_MMA2("f16"); else BSRP_MMA2("tf32");
+    } else if constexpr (NSTEP == 4) {
+        if constexpr (KIND == 1) BSRP_MMA4("f16"); else BSRP_MMA4("tf32");
+    } else {
+        static_assert(NSTEP % 4 == 0, "k steps per block");
+#pragma unroll
+        for (int s = 0; s < NSTEP; s += 4)
+            tc_mma_run<KIND, 4, AK, BK>(d_tmem, a_desc + (uint64_t)(s * AK), b_desc + (uint64_t)(s * BK), idesc);
+    }
+}
+#undef BSRP_MMA2
+#undef BSRP_MMA4
+
+// tcgen05.mma issued by one elected lane of a converged warp; the 64-bit
+// descriptors are assembled from 32-bit halves inside PTX.  Every operand is
+// warp-uniform, so ptxas keeps them in uniform registers.
+template <int KIND>
+__device__ __forceinline__ void tc_mma_elect(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                             uint32_t b_hi, uint32_t idesc) {
+    if constexpr (KIND == 1) {
+        asm volatile(
+            "{\n.reg .pred p;\n.reg .b64 a, b;\nmov.b64 a, {%1, %2};\nmov.b64 b, {%3, %4};\n"
+            "elect.sync _|p, 0xffffffff;\n"
+            "@p tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, 1;\n}\n" ::"r"(d_tmem),
+            "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc));
+    } else {
+        asm volatile(
+            "{\n.reg .pred p;\n.reg .b64 a, b;\nmov.b64 a, {%1, %2};\nmov.b64 b, {%3, %4};\n"
+            "elect.sync _|p, 0xffffffff;\n"
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], a, b, %5, 1;\n}\n" ::"r"(d_tmem),
+            "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc));
+    }
+}
+
 // UMMA shared-memory matrix descriptor (sm_100): start, leading-byte offset
 // (stride between MN atoms for swizzled MN-major), stride-byte offset (between
 // 8-row K groups), version 1, swizzle layout type.
@@ -202,7 +262,7 @@ struct Cfg {
     static constexpr uint32_t B_LAYOUT = TF32 ? 1u : BW == 128 ? 2u : BW == 64 ? 4u : 6u;  // SW128_32B / SW128 / SW64 / SW32
     static_assert(!TF32 || BW == 128, "tf32 MN-major operands need 128-byte block rows (b >= 32)");
     static constexpr int MAX_RUN = 256 / B;                 // blocks per MMA (N <= 256)
-    static constexpr int G = BLOCK_BYTES >= 8192 ? 1 : BLOCK_BYTES >= 4096 ? 2 : 4;  // blocks per B TMA
+    static constexpr int G = BLOCK_BYTES >= 8192 ? 1 : BLOCK_BYTES >= 2048 ? 4 : 8;  // blocks per B TMA
 };
 
 #ifdef WGRAD_TRACE
@@ -237,8 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *ringA = smem;
     uint8_t *ringB = ringA + (size_t)p.stages * C::A_BYTES;
-    uint2 *meta = reinterpret_cast<uint2 *>(ringB + (size_t)p.nbslots * C::BLOCK_BYTES);
-    uint32_t *s_used = reinterpret_cast<uint32_t *>(meta + p.stages * kMetaPairs);
+    uint4 *meta = reinterpret_cast<uint4 *>(ringB + (size_t)p.nbslots * C::BLOCK_BYTES);
+    uint32_t *s_used = reinterpret_cast<uint32_t *>(meta + p.stages * kMetaQuads);
     uint64_t *full = reinterpret_cast<uint64_t *>(s_used + ((p.stages + 1) & ~1));
     uint64_t *empty = full + p.stages;
     uint64_t *accfull = empty + p.stages;
@@ -264,8 +324,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nbc = (int)(p.K / B);
     const int J0 = kr * p.kr_blocks;
     const int nbJ = min(p.kr_blocks, nbc - J0);
+    // two MMA warps share the issue work: warp 1 owns block columns [0, jhalf), warp 2 the rest
+    const int jhalf = (nbJ + 1) / 2;
     const int64_t Ib = (int64_t)split * p.nbr / p.nsplit, Ie = (int64_t)(split + 1) * p.nbr / p.nsplit;
-    const int nchunks = (int)((Ie - Ib + p.chunk_rows - 1) / p.chunk_rows);
+    // chunk 0 is short (32 rows) so the first plan is ready early; later chunks are chunk_rows long
+    const int first_rows = min(32, p.chunk_rows);
+    const int64_t nrows_cta = Ie - Ib;
+    const int nchunks = nrows_cta <= first_rows ? (nrows_cta > 0 ? 1 : 0)
+                                                : 1 + (int)((nrows_cta - first_rows + p.chunk_rows - 1) / p.chunk_rows);
+    auto chunk_start = [&](int c) -> int64_t { return c == 0 ? Ib : Ib + first_rows + (int64_t)(c - 1) * p.chunk_rows; };
+    auto chunk_len = [&](int c) -> int {
+        return (int)min((int64_t)(c == 0 ? first_rows : p.chunk_rows), Ie - chunk_start(c));
+    };
     if (threadIdx.x == 0) TRACE(0);
 
     if (warp == 0 && lane == 0) {
@@ -274,13 +344,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
+            mbar_init(full + s, 2);   // A producer + B producer
+            mbar_init(empty + s, 2);  // one commit from each MMA warp
         }
-        mbar_init(accfull, 1);
+        mbar_init(accfull, 2);
         for (int i = 0; i < 2; ++i) {
             mbar_init(plan_full + i, 1);
-            mbar_init(plan_empty + i, 1);
+            mbar_init(plan_empty + i, 2);  // both producers release a plan chunk
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -307,8 +377,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // per-row arithmetic.
         for (int c = 0; c < nchunks; ++c) {
             const int buf = c & 1;
-            const int64_t Ic = Ib + (int64_t)c * p.chunk_rows;
-            const int nrow = (int)min((int64_t)p.chunk_rows, Ie - Ic);
+            const int64_t Ic = chunk_start(c);
+            const int nrow = chunk_len(c);
             for (int i = lane; i <= nrow; i += 32) s_rp[i] = __ldg(p.rowptr + Ic + i);
             __syncwarp();
             const int base = s_rp[0], total = s_rp[nrow] - base;
@@ -334,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int jprev = -2, rlen = 0;
                     for (int q = 0; q < cnt; ++q) {
                         const int J = (int)s_col[q0 + q] - J0;
-                        if (J == jprev + 1 && rlen < C::MAX_RUN) {
+                        if (J == jprev + 1 && rlen < C::MAX_RUN && J != jhalf) {
                             ++rlen;
                         } else {
                             ++nruns;
@@ -356,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int jprev = -2, rlen = 0, rstart = 0, k = off;
                     for (int q = 0; q < cnt; ++q) {
                         const int J = (int)s_col[q0 + q] - J0;
-                        if (J == jprev + 1 && rlen < C::MAX_RUN) {
+                        if (J == jprev + 1 && rlen < C::MAX_RUN && J != jhalf) {
                             ++rlen;
                         } else {
                             if (rlen)
@@ -382,105 +452,169 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < nbJ * B; c += 16) tmem_st16_zero(tmem + lane_base + c);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
-    if (warp == 1 || warp >= 4) {  // the MMA warp starts only after the accumulator is zeroed
+    if (warp == 1 || warp == 2 || warp >= 4) {  // the MMA warps start only after the accumulator is zeroed
         tc_fence_before();
-        asm volatile("bar.sync 1, 160;" ::: "memory");
+        asm volatile("bar.sync 1, 192;" ::: "memory");
         tc_fence_after();
     }
 
-    if (warp == 0 && lane == 0) {
-        // ------------------------------------------------ TMA producer (one thread)
-        // Stage s of the A ring holds one block row's b x 128 dY slab (one 3-D TMA);
-        // its kept blocks take consecutive slots of the B ring (never wrapping: a
-        // row that would wrap starts at slot 0 and the tail slots are skipped),
-        // loaded G blocks per 4-D TMA.  Stages and slots are reclaimed in issue
-        // order as the MMA commits arrive.
-        int head = 0, tail = 0, in_flight = 0, bhead = 0, bfree = p.nbslots, nrows_tr = 0;
-        (void)nrows_tr;
-        uint32_t tail_ph = 0;
+    if ((warp == 0 || warp == 4) && lane == 0) {
+        // ------------------------------------------------ TMA producers (one thread each)
+        // Both walk the same sequence of kept block rows (row j uses stage j % stages).
+        // Warp 0 loads row j's b x 128 dY slab (one 3-D TMA) into the A ring; warp 4
+        // (an epilogue warp, idle until the accumulator is final) places the row's
+        // kept blocks in consecutive B-ring slots (never wrapping: a row that would
+        // wrap starts at slot 0 and the tail slots are skipped), loads them G blocks
+        // per 4-D TMA and writes the stage's ready-to-issue MMA runs.  `full` needs
+        // both arrivals plus all bytes; stages and slots are reclaimed in order as
+        // the MMA commits arrive on `empty`.
+        const bool is_a = warp == 0;
+        int j = 0;  // kept rows issued so far
+        int tail = 0, bhead = 0, bfree = p.nbslots;
         const uint32_t sA0 = smem_u32(ringA), sB0 = smem_u32(ringB);
-        TRACE(1);
+        const uint32_t b_lo0 = (uint32_t)smem_desc(sB0, C::B_LBO, C::B_SBO, C::B_LAYOUT);
+        long long cyc_wait = 0, cyc_issue = 0, cyc_start = clock64();
+        (void)cyc_wait; (void)cyc_issue; (void)cyc_start;
         for (int c = 0; c < nchunks; ++c) {
             const int buf = c & 1;
-            const int64_t Ic = Ib + (int64_t)c * p.chunk_rows;
-            const int nrow = (int)min((int64_t)p.chunk_rows, Ie - Ic);
+            const int64_t Ic = chunk_start(c);
+            const int nrow = chunk_len(c);
             mbar_wait(plan_full + buf, (c >> 1) & 1);
-            if (c == 0) TRACE(205);
             const int4 *rows = s_rows + buf * kRowCap;
             const uint2 *runs = s_runs + buf * kColCap;
             for (int r = 0; r < nrow; ++r) {
                 const int4 rr = rows[r];
                 const int cnt = rr.x & 0xFFFF;
                 if (cnt == 0) continue;
-                const int nruns = rr.x >> 16, need = rr.y;
-                const int waste = bhead + need > p.nbslots ? p.nbslots - bhead : 0;
-                while (in_flight == p.stages || bfree < need + waste) {  // reclaim the oldest stage
-                    mbar_wait(empty + tail, tail_ph);
-                    bfree += (int)s_used[tail];
-                    if (++tail == p.stages) { tail = 0; tail_ph ^= 1; }
-                    --in_flight;
-                }
-                const int slot0 = waste ? 0 : bhead;
-                uint2 *m = meta + head * kMetaPairs;
-                m[0] = make_uint2((uint32_t)nruns, (uint32_t)slot0);
-                for (int i = 0; i < nruns; ++i) m[1 + i] = runs[rr.z + i];
-                s_used[head] = (uint32_t)(need + waste);
-                if (WGRAD_TRACE_MODE & 1) {
-                    mbar_arrive(full + head);
+                const int stage = j % p.stages;
+#ifdef WGRAD_TRACE
+                const long long tw0 = clock64();
+#endif
+                if (is_a) {
+                    if (j >= p.stages) mbar_wait(empty + stage, (uint32_t)((j / p.stages) - 1) & 1u);
                 } else {
-                    mbar_arrive_expect_tx(full + head, (uint32_t)(C::A_BYTES + need * C::BLOCK_BYTES));
-                    tma_load_3d(&tm_dy, full + head, sA0 + head * C::A_BYTES, 0, (int)(Ic + r) * B, n0 / C::AW);
+                    const int need = rr.y;
+                    const int waste = bhead + need > p.nbslots ? p.nbslots - bhead : 0;
+                    while (j - tail >= p.stages || bfree < need + waste) {  // reclaim the oldest row
+                        mbar_wait(empty + tail % p.stages, (uint32_t)(tail / p.stages) & 1u);
+                        bfree += (int)s_used[tail % p.stages];
+                        ++tail;
+                    }
+                    const int slot0 = waste ? 0 : bhead;
+                    s_used[stage] = (uint32_t)(need + waste);
+                    bhead = slot0 + need;
+                    if (bhead == p.nbslots) bhead = 0;
+                    bfree -= need + waste;
+                    // ready-to-issue runs: TMEM address, B descriptor low word, instruction descriptor
+                    const int nruns = rr.x >> 16;
+                    uint4 *m = meta + stage * kMetaQuads;
+                    const uint32_t slot_lo = b_lo0 + (uint32_t)((slot0 * C::BLOCK_BYTES) >> 4);
+                    for (int i = 0; i < nruns; ++i) {
+                        const uint2 run = runs[rr.z + i];
+                        m[1 + i] = make_uint4(tmem + (run.x & 0xFFFFu), slot_lo + (((run.x >> 16) * C::BLOCK_BYTES) >> 4),
+                                              run.y, 0u);
+                    }
+                    m[0] = make_uint4((uint32_t)nruns, 0u, 0u, 0u);
+#ifdef WGRAD_TRACE
+                    const long long tw1 = clock64();
+                    cyc_wait += tw1 - tw0;
+#endif
+                    mbar_arrive_expect_tx(full + stage, (uint32_t)(need * C::BLOCK_BYTES));
                     for (int g = 0; g < need; g += C::G)
-                        tma_load_4d(&tm_val, full + head, sB0 + (slot0 + g) * C::BLOCK_BYTES, 0, 0, 0, rr.w + g);
+                        tma_load_4d(&tm_val, full + stage, sB0 + (slot0 + g) * C::BLOCK_BYTES, 0, 0, 0, rr.w + g);
+#ifdef WGRAD_TRACE
+                    cyc_issue += clock64() - tw1;
+#endif
                 }
-                if (nrows_tr < 100) TRACE(2 + nrows_tr);
-                ++nrows_tr;
-                bhead = slot0 + need;
-                if (bhead == p.nbslots) bhead = 0;
-                bfree -= need + waste;
-                ++in_flight;
-                if (++head == p.stages) head = 0;
+                if (is_a) {
+#ifdef WGRAD_TRACE
+                    const long long tw1 = clock64();
+                    cyc_wait += tw1 - tw0;
+#endif
+                    mbar_arrive_expect_tx(full + stage, (uint32_t)C::A_BYTES);
+                    tma_load_3d(&tm_dy, full + stage, sA0 + stage * C::A_BYTES, 0, (int)(Ic + r) * B, n0 / C::AW);
+#ifdef WGRAD_TRACE
+                    cyc_issue += clock64() - tw1;
+#endif
+                }
+                ++j;
             }
             mbar_arrive(plan_empty + buf);
         }
-        while (in_flight == p.stages) {  // the end marker needs a free stage
-            mbar_wait(empty + tail, tail_ph);
-            if (++tail == p.stages) { tail = 0; tail_ph ^= 1; }
-            --in_flight;
-        }
-        meta[head * kMetaPairs] = make_uint2(kEndMarker, 0);
-        mbar_arrive(full + head);
-    } else if (warp == 1 && lane == 0) {
-        // ------------------------------------------------ MMA issuer (one thread)
+#ifdef WGRAD_TRACE
+        g_trace[blockIdx.x][210 + 4 * (warp == 4)] = (unsigned long long)cyc_wait;
+        g_trace[blockIdx.x][211 + 4 * (warp == 4)] = (unsigned long long)cyc_issue;
+        g_trace[blockIdx.x][212 + 4 * (warp == 4)] = (unsigned long long)(clock64() - cyc_start);
+        g_trace[blockIdx.x][213 + 4 * (warp == 4)] = (unsigned long long)j;
+#endif
+        // end marker in stage j % stages: free it, then both producers arrive (no bytes)
+        const int stage = j % p.stages;
+        if (j >= p.stages) mbar_wait(empty + stage, (uint32_t)((j / p.stages) - 1) & 1u);
+        if (!is_a) meta[stage * kMetaQuads] = make_uint4(kEndMarker, 0u, 0u, 0u);
+        mbar_arrive(full + stage);
+    } else if (warp == 1 || warp == 2) {
+        // ------------------------------------------------ MMA issuers (whole warps, one elected lane each)
+        // Warp 1 issues the runs in block columns [0, jhalf), warp 2 the rest:
+        // disjoint TMEM columns, so the two issue streams need no ordering; each
+        // commits to every stage's `empty` barrier (count 2) and to `accfull`.
+        // Every lane reads the same ready-to-issue run words; redux.sync makes them
+        // warp-uniform, so each tcgen05.mma is one predicated UTCHMMA.
         const uint64_t a_desc0 = smem_desc(smem_u32(ringA), C::A_LBO, C::A_SBO, C::A_LAYOUT);
-        const uint64_t b_desc0 = smem_desc(smem_u32(ringB), C::B_LBO, C::B_SBO, C::B_LAYOUT);
-        int stage = 0, nmma_tr = 0;
-        (void)nmma_tr;
+        const uint32_t a_lo0 = (uint32_t)a_desc0, a_hi = (uint32_t)(a_desc0 >> 32);
+        const uint32_t b_hi = (uint32_t)(smem_desc(smem_u32(ringB), C::B_LBO, C::B_SBO, C::B_LAYOUT) >> 32);
+        const uint32_t col_split = tmem + (uint32_t)(jhalf * B);
+        int stage = 0;
         uint32_t phase = 0;
+        long long mw = 0, mi = 0, m_start = clock64();
+        (void)mw; (void)mi; (void)m_start;
         for (;;) {
+#ifdef WGRAD_TRACE
+            const long long t0m = clock64();
+#endif
             mbar_wait(full + stage, phase);
             tc_fence_after();
-            if (nmma_tr < 100) TRACE(102 + nmma_tr);
-            ++nmma_tr;
-            const uint2 *m = meta + stage * kMetaPairs;
-            const uint2 m0 = m[0];
-            if (m0.x == kEndMarker) break;
-            const uint64_t a_desc = a_desc0 + (uint64_t)((stage * C::A_BYTES) >> 4);
-            const uint64_t b_base = b_desc0 + (uint64_t)((m0.y * C::BLOCK_BYTES) >> 4);
-            for (uint32_t i = 0; i < m0.x; ++i) {
-                const uint2 run = m[1 + i];
-                const uint64_t b_desc = b_base + (uint64_t)(((run.x >> 16) * C::BLOCK_BYTES) >> 4);
-                const uint32_t d = tmem + (run.x & 0xFFFFu);
+#ifdef WGRAD_TRACE
+            const long long t1m = clock64();
+            mw += t1m - t0m;
+#endif
+            const uint4 *m = meta + stage * kMetaQuads;
+            const uint32_t nruns = __reduce_or_sync(0xffffffffu, m[0].x);
+            if (nruns == kEndMarker) break;
+            const uint32_t a_lo = a_lo0 + (uint32_t)((stage * C::A_BYTES) >> 4);
+            for (uint32_t i = 0; i < nruns; ++i) {
+                const uint4 w = m[1 + i];
+                const uint32_t d = __reduce_or_sync(0xffffffffu, w.x);
+                if ((d < col_split) != (warp == 1)) continue;
+                const uint32_t b_lo = __reduce_or_sync(0xffffffffu, w.y);
+                const uint32_t idesc = __reduce_or_sync(0xffffffffu, w.z);
 #pragma unroll
                 for (int s = 0; s < B / C::UK; ++s)
-                    if (!(WGRAD_TRACE_MODE & 2)) tc_mma<KIND>(d, a_desc + (uint64_t)((s * C::A_KSTEP) >> 4), b_desc + (uint64_t)((s * C::B_KSTEP) >> 4),
-                                 run.y, 1u);
+                    if (!(WGRAD_TRACE_MODE & 2))
+                        tc_mma_elect<KIND>(d, a_lo + ((s * C::A_KSTEP) >> 4), a_hi, b_lo + ((s * C::B_KSTEP) >> 4), b_hi,
+                                           idesc);
             }
-            tc_commit(empty + stage);  // frees the stage (and its B slots) once these MMAs complete
+            __syncwarp();
+            if (lane == 0) {
+                if (WGRAD_TRACE_MODE & 4) mbar_arrive(empty + stage); else
+                tc_commit(empty + stage);  // frees the stage (and its B slots) once these MMAs complete
+            }
+            __syncwarp();
+#ifdef WGRAD_TRACE
+            mi += clock64() - t1m;
+#endif
             if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
-        tc_commit(accfull);
-    } else if (warp >= 4) {
+#ifdef WGRAD_TRACE
+        if (lane == 0) {
+            g_trace[blockIdx.x][218 + 3 * (warp - 1)] = (unsigned long long)mw;
+            g_trace[blockIdx.x][219 + 3 * (warp - 1)] = (unsigned long long)mi;
+            g_trace[blockIdx.x][220 + 3 * (warp - 1)] = (unsigned long long)(clock64() - m_start);
+        }
+#endif
+        if (lane == 0) tc_commit(accfull);
+    }
+    if (warp >= 4) {
+        __syncwarp();  // warp 4's lane 0 rejoins after its B-producer loop
         // ------------------------------------------------ epilogue
         // TMEM -> registers -> a [32 kcol][128 n] fp32 staging tile in the (now
         // idle) A ring -> one TMA bulk tensor store (or reduce-add) per 16 kcols.
@@ -542,13 +676,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // dW (+)= sum over splits of the partial tiles, in split order (deterministic).
+// Each thread owns float4 column blocks; up to 16 split loads are issued ahead
+// of the (ordered) adds so the L2-resident partials stream at full rate.
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4 *__restrict__ ws, float4 *__restrict__ dW,
                                                             int64_t n4, int nsplit, int accumulate) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
         float4 a = accumulate ? dW[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s = 0; s < nsplit; ++s) {
-            const float4 v = __ldcs(ws + (size_t)s * n4 + i);
-            a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+        for (int s = 0; s < nsplit; s += 16) {  // up to 16 independent loads in flight, then ordered adds
+            float4 v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (s + u < nsplit) v[u] = __ldcs(ws + (size_t)(s + u) * n4 + i);
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (s + u < nsplit) {
+                    a.x += v[u].x; a.y += v[u].y; a.z += v[u].z; a.w += v[u].w;
+                }
         }
         dW[i] = a;
     }
@@ -689,6 +832,12 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     p.chunk_rows = pl.chunk_rows;
     p.ws = ws;
     p.mode = pl.nsplit > 1 ? 3 : accumulate ? 1 : 0;
+#ifdef WGRAD_TMA_REDUCE
+    if (pl.nsplit > 1) {  // experiment: TMA bulk reduce-add of every split into dW
+        p.mode = 1;
+        if (!accumulate) cudaMemsetAsync(dW, 0, (size_t)K * N * 4, stream);
+    }
+#endif
     auto kern = wgrad_tc_kernel<KIND, B>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     if (e != cudaSuccess) return e;
@@ -696,9 +845,9 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     kern<<<grid, kThreads, pl.smem, stream>>>(tm_dy, tm_val, tm_dw, tm_ws, p);
     count_launch();
     e = cudaGetLastError();
-    if (e != cudaSuccess || pl.nsplit == 1) return e;
+    if (e != cudaSuccess || pl.nsplit == 1 || p.mode == 1) return e;
     const int64_t n4 = K * N / 4;
-    const unsigned rgrid = (unsigned)std::min<int64_t>((n4 + 255) / 256, sms * 8);
+    const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 8));
     splitk_reduce_kernel<<<rgrid, 256, 0, stream>>>(reinterpret_cast<const float4 *>(ws),
                                                     reinterpret_cast<float4 *>(dW), n4, pl.nsplit, accumulate);
     count_launch();

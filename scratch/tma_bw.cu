@@ -30,8 +30,12 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap *tm, uint64_t *bar
 }
 
 // CTA c handles column tile (c % ntn) of width tile_cols, rows [r0, r1) in steps of `rows`.
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap *tm, uint64_t *bar, void *dst, int x, int y, int z) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                 ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)) : "memory");
+}
 __global__ void stream_kernel(const __grid_constant__ CUtensorMap tm, int ntn, int tile_cols, int box_cols, int rows,
-                              int M, int nsplit, int S, int stage_bytes) {
+                              int M, int nsplit, int S, int stage_bytes, int use3d) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *full = (uint64_t *)(smem + S * stage_bytes);
@@ -50,6 +54,8 @@ __global__ void stream_kernel(const __grid_constant__ CUtensorMap tm, int ntn, i
         for (int I = Ib; I < Ie; ++I) {
             mbar_wait(empty + st, ph ^ 1);
             mbar_arrive_expect_tx(full + st, stage_bytes);
+            if (use3d & 1) tma_load_3d(&tm, full + st, smem + st * stage_bytes, 0, I * rows, nt * nbox);
+            else
             for (int a = 0; a < nbox; ++a)
                 tma_load_2d(&tm, full + st, smem + st * stage_bytes + a * (box_cols * 4 * rows), nt * tile_cols + a * box_cols, I * rows);
             if (++st == S) { st = 0; ph ^= 1; }
@@ -58,7 +64,10 @@ __global__ void stream_kernel(const __grid_constant__ CUtensorMap tm, int ntn, i
         int st = 0; uint32_t ph = 0;
         for (int I = Ib; I < Ie; ++I) {
             mbar_wait(full + st, ph);
-            mbar_arrive(empty + st);
+            if (use3d & 2)
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(empty + st)) : "memory");
+            else
+                mbar_arrive(empty + st);
             if (++st == S) { st = 0; ph ^= 1; }
         }
     }
@@ -73,8 +82,9 @@ int main() {
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
     auto enc = (PFN_cuTensorMapEncodeTiled_v12000)f;
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    struct Cfg { int tile_cols, box_cols, rows, S, swz; };
+    struct Cfg { int tile_cols, box_cols, rows, S, swz, use3d = 0; };
     std::vector<Cfg> cfgs = {
+        {128, 32, 32, 4, 4, 1}, {128, 32, 32, 4, 4, 3}, {128, 32, 32, 8, 4, 1}, {128, 32, 32, 8, 4, 3},
         {128, 32, 32, 3, 4}, {128, 32, 32, 6, 4}, {128, 32, 32, 12, 4}, {128, 32, 32, 12, 0},
         {128, 32, 64, 6, 4}, {128, 32, 128, 3, 4}, {256, 32, 32, 6, 4}, {512, 32, 32, 4, 4},
         {1536, 32, 8, 4, 4}, {1536, 32, 16, 4, 4}, {128, 128, 32, 6, 0}, {128, 64, 32, 6, 0},
@@ -84,8 +94,14 @@ int main() {
         cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M * 3};
         cuuint64_t str[1] = {(cuuint64_t)N * 4};
         cuuint32_t box[2] = {(cuuint32_t)c.box_cols, (cuuint32_t)c.rows};
-        cuuint32_t es[2] = {1, 1};
-        CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        cuuint32_t es[3] = {1, 1, 1};
+        cuuint64_t dims3[3] = {(cuuint64_t)c.box_cols, (cuuint64_t)M * 3, (cuuint64_t)N / c.box_cols};
+        cuuint64_t str3[2] = {(cuuint64_t)N * 4, (cuuint64_t)c.box_cols * 4};
+        cuuint32_t box3[3] = {(cuuint32_t)c.box_cols, (cuuint32_t)c.rows, (cuuint32_t)(c.tile_cols / c.box_cols)};
+        CUresult r = (c.use3d & 1) ? enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d, dims3, str3, box3, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         c.swz == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) :
+            enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          c.swz == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) { printf("encode failed %d\n", r); continue; }
@@ -102,7 +118,7 @@ int main() {
             CUtensorMap tm2 = tm;  // use the same map, shifted rows not needed: region size 3M; use M rows at offset
             (void)base;
             cudaEventRecord(e0);
-            stream_kernel<<<ntn * nsplit, 64, smem>>>(tm2, ntn, c.tile_cols, c.box_cols, c.rows, M, nsplit, c.S, stage_bytes);
+            stream_kernel<<<ntn * nsplit, 64, smem>>>(tm2, ntn, c.tile_cols, c.box_cols, c.rows, M, nsplit, c.S, stage_bytes, c.use3d);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -110,7 +126,7 @@ int main() {
         }
         cudaError_t err = cudaGetLastError();
         double gb = (double)M * N * 4 / 1e9;
-        printf("tile %4d box %3dx%3d S=%2d swz=%d grid=%d: %.1f us  %.0f GB/s  %s\n", c.tile_cols, c.box_cols, c.rows, c.S,
+        printf("3d=%d tile %4d box %3dx%3d S=%2d swz=%d grid=%d: %.1f us  %.0f GB/s  %s\n", c.use3d, c.tile_cols, c.box_cols, c.rows, c.S,
                c.swz, ntn * nsplit, best * 1e3, gb / (best * 1e-3), cudaGetErrorString(err));
     }
     return 0;

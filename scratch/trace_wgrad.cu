@@ -47,12 +47,39 @@ int main(int argc, char **argv) {
 #ifdef NO_TRACE
     return 0;
 #endif
+    {
+        cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+        const int64_t n4 = (int64_t)K * N / 4;
+        for (int rep = 0; rep < 3; ++rep) {
+            cudaEventRecord(e0);
+            bsrp::tc::splitk_reduce_kernel<<<576, 256>>>((const float4 *)ws, (float4 *)dW, n4, 12, 0);
+            cudaEventRecord(e1); cudaEventSynchronize(e1);
+            float ms; cudaEventElapsedTime(&ms, e0, e1);
+            printf("reduce alone: %.1f us\n", ms * 1e3);
+        }
+    }
     static unsigned long long tr[160][256];
 #ifndef NO_TRACE
     cudaMemcpyFromSymbol(tr, bsrp::tc::g_trace, sizeof tr);
 #endif
     unsigned long long t0 = ~0ull;
     for (int c = 0; c < 144; ++c) t0 = std::min(t0, tr[c][0]);
+    {
+        unsigned long long emax = 0, smax = 0, plmax = 0; double loopsum = 0;
+        int nC = 0;
+        for (int c = 0; c < 160; ++c) if (tr[c][0]) {
+            emax = std::max(emax, tr[c][204]); smax = std::max(smax, tr[c][0]); plmax = std::max(plmax, tr[c][205]);
+            loopsum += (double)(tr[c][203] - tr[c][205]); ++nC;
+        }
+        printf("CTAs %d: last start %.2f  last plan %.2f  last end %.2f  mean main loop %.2f us\n", nC, (smax - t0) / 1e3, (plmax - t0) / 1e3, (emax - t0) / 1e3, loopsum / nC / 1e3);
+    }
+    {
+        double v[16] = {0}; double rows = 0; int n = 0;
+        for (int c = 0; c < 160; ++c) if (tr[c][0]) { for (int k = 0; k < 16; ++k) v[k] += tr[c][210 + k]; rows += tr[c][213]; ++n; }
+        printf("A producer per row (cyc): wait %.0f issue %.0f total %.0f (rows/CTA %.1f)\n", v[0] / rows, v[1] / rows, v[2] / rows, rows / n);
+        printf("B producer per row (cyc): wait %.0f issue %.0f total %.0f\n", v[4] / rows, v[5] / rows, v[6] / rows);
+        printf("mma warp1 per row: wait %.0f issue %.0f total %.0f | warp2 wait %.0f issue %.0f\n", v[8] / rows, v[9] / rows, v[10] / rows, v[11] / rows, v[12] / rows);
+    }
     for (int c : {0, 1, 12, 77, 143}) {
         printf("CTA %d: start %.2f  prod %.2f plan %.2f  epi %.2f..%.2f\n", c, (tr[c][0] - t0) / 1e3, (tr[c][1] - t0) / 1e3, (tr[c][205] - t0) / 1e3, (tr[c][203] - t0) / 1e3, (tr[c][204] - t0) / 1e3);
         printf("  TMA issue :"); for (int r = 0; r < 20; r += 1) printf(" %.2f", (tr[c][2 + r] - t0) / 1e3); printf("\n");
