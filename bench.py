@@ -302,63 +302,66 @@ def run_native(a):
     lib = bp._lib.load()
     launches_per_step = {}
     use_graph = not a.no_graph
-    graphs = None
+    step_graphs, phase_graphs = None, None
+    REP = 4  # launches of one phase per input set inside a per-kernel timing graph
+
+    def full_step(j):
+        for p in phases:
+            phase_fn(j, p)()
+
     if use_graph:
         try:
-            graphs = []
             s = torch.cuda.Stream(device=dev)
             s.wait_stream(torch.cuda.current_stream())
+            # one graph per input set holding the whole step (prune -> wgrad -> decompress)
+            step_graphs = []
             for j in range(NSETS):
-                gj = {}
-                for p in phases:
-                    g = torch.cuda.CUDAGraph()
-                    n0 = lib.bsr_kernel_launches()
-                    with torch.cuda.graph(g, stream=s):
-                        phase_fn(j, p)()
-                    launches_per_step[p] = lib.bsr_kernel_launches() - n0
-                    gj[p] = g
-                graphs.append(gj)
+                g = torch.cuda.CUDAGraph()
+                n0 = lib.bsr_kernel_launches()
+                with torch.cuda.graph(g, stream=s):
+                    full_step(j)
+                step_graphs.append(g)
+                launches_per_step["step"] = lib.bsr_kernel_launches() - n0
+            # per-kernel timing graphs: REP x NSETS back-to-back launches of one phase
+            phase_graphs = {}
+            for p in phases:
+                g = torch.cuda.CUDAGraph()
+                n0 = lib.bsr_kernel_launches()
+                with torch.cuda.graph(g, stream=s):
+                    for _ in range(REP):
+                        for j in range(NSETS):
+                            phase_fn(j, p)()
+                launches_per_step[p] = (lib.bsr_kernel_launches() - n0) // (REP * NSETS)
+                phase_graphs[p] = g
             torch.cuda.current_stream().wait_stream(s)
             for j in range(NSETS):
-                for p in phases:
-                    graphs[j][p].replay()
+                step_graphs[j].replay()
             torch.cuda.synchronize()
-            # the replays reproduce the eager result exactly (same kernels, same inputs)
-            # (split-K dW tiles are summed with atomics, so dW may differ in the last bits)
+            # the replays reproduce the eager result (dW: split-K partials summed in split order)
             if not torch.equal(bsrs[0].colidx, ref_colidx):
                 raise RuntimeError("graph replay prune differs from eager launch")
             if not torch.allclose(dWs[0], ref_dw, rtol=1e-4, atol=1e-6):
                 raise RuntimeError("graph replay dW differs from eager launch")
         except Exception as e:  # capture unsupported: launch eagerly
             print(f"note: CUDA-graph capture failed ({e!r}); launching eagerly", file=sys.stderr)
-            use_graph, graphs = False, None
+            use_graph, step_graphs, phase_graphs = False, None, None
     if not use_graph:
         for p in phases:
             n0 = lib.bsr_kernel_launches()
             phase_fn(0, p)()
             launches_per_step[p] = lib.bsr_kernel_launches() - n0
+        launches_per_step["step"] = sum(launches_per_step[p] for p in phases)
         torch.cuda.synchronize()
 
-    def run_phase(j, p):
-        if use_graph:
-            graphs[j][p].replay()
-        else:
-            phase_fn(j, p)()
-
     stream = torch.cuda.current_stream()
-    nph = len(phases) + (1 if world > 1 else 0)
 
-    def step(j, evs=None):
-        for i, p in enumerate(phases):
-            if evs is not None:
-                evs[i].record(stream)
-            run_phase(j, p)
+    def step(j):
+        if use_graph:
+            step_graphs[j].replay()
+        else:
+            full_step(j)
         if world > 1:
-            if evs is not None:
-                evs[len(phases)].record(stream)
             D.allreduce_dw(dWs[j])
-        if evs is not None:
-            evs[nph].record(stream)
 
     for i in range(a.warmup):
         step(i % NSETS)
@@ -368,7 +371,7 @@ def run_native(a):
     r_ne = int((bsrs[0].rowptr[1:] != bsrs[0].rowptr[:-1]).sum().item())
     work = metrics.step_work(M, K, N, b, k, s_x, s_dy, r_ne)
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nph + 1)] for _ in range(a.steps)]
+    # ---- the timed region: K whole steps, barrier + synchronize on both sides, clocks sampled
     t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clk = ClockSampler(local)
     D.barrier()
@@ -376,7 +379,7 @@ def run_native(a):
     clk.start()
     t0e.record(stream)
     for i in range(a.steps):
-        step(i % NSETS, evs[i])
+        step(i % NSETS)
     t1e.record(stream)
     while not t1e.query():  # the GPU is still busy: keep sampling clocks
         time.sleep(0.0005)
@@ -385,12 +388,39 @@ def run_native(a):
     D.barrier()
     t_ms = t0e.elapsed_time(t1e)
     t_ms_max = D.max_over_ranks(t_ms, dev)
-    ph_ms = {}
-    for i, p in enumerate(phases + (["allreduce"] if world > 1 else [])):
-        ph_ms[p] = statistics.fmean(evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(a.steps))
     bytes_all = D.sum_over_ranks(work.bytes, dev) * a.steps
     flops_all = D.sum_over_ranks(work.wgrad_flops, dev) * a.steps
     value = bytes_all / (t_ms_max * 1e-3) / 1e9
+
+    # ---- per-kernel durations: each phase launched back to back (REP x NSETS launches per
+    # graph replay, rotating input sets), CUDA events on the launching stream around the replays
+    ph_ms = {}
+    n_rep = max(3, min(200, a.steps // 4))
+    for p in phases:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if use_graph:
+            phase_graphs[p].replay()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(n_rep):
+            if use_graph:
+                phase_graphs[p].replay()
+            else:
+                for _ in range(REP):
+                    for j in range(NSETS):
+                        phase_fn(j, p)()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ph_ms[p] = e0.elapsed_time(e1) / (n_rep * REP * NSETS)
+    if world > 1:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        D.barrier()
+        e0.record(stream)
+        for i in range(n_rep):
+            D.allreduce_dw(dWs[i % NSETS])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ph_ms["allreduce"] = D.max_over_ranks(e0.elapsed_time(e1) / n_rep, dev)
 
     # ---- e2e: the public API with host buffers; H2D of the step's inputs and D2H of dW timed
     pin_X = torch.from_numpy(Xh.view(np.int16) if a.dtype == "bf16" else Xh).pin_memory()
@@ -465,7 +495,7 @@ def run_native(a):
                  "launch_ms": dk["ms"], "peak_source": f"{pk['source']} (MEASURED_PEAKS.json)"
                  if pk["source"] == "measured" else "fallback (B200_PROFILING.md)"})
 
-    per_step_launches = sum(launches_per_step.values())
+    per_step_launches = launches_per_step["step"]
     out = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": t_ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -480,7 +510,9 @@ def run_native(a):
                             "bsr_bytes": metrics.bsr_bytes(M, b, k, s_x)},
         "work_per_step": {"alg_bytes": work.bytes, "wgrad_flops": work.wgrad_flops, "k": k, "nblocks": nblocks,
                           "r_ne": r_ne, "wgrad_flops_all_ranks_per_s": flops_all / (t_ms_max * 1e-3)},
-        "launch": "cuda-graph replays per phase" if use_graph else "eager",
+        "launch": "one CUDA graph per step (prune -> wgrad -> decompress)" if use_graph else "eager",
+        "kernel_timing": "per phase: back-to-back launches inside one graph over the rotating input sets, "
+                         "CUDA events around the replays (a second timed region after the step loop)",
         "gpu_launches": per_step_launches * a.steps,
         "gpu_launches_per_step": launches_per_step,
         "clocks": clk.summary(),

@@ -169,6 +169,13 @@ __device__ __forceinline__ void select_bin(const uint32_t *hist, int nbins, uint
     __syncthreads();
 }
 
+#ifdef PRUNE_TRACE
+__device__ unsigned long long g_ptrace[2048][8];
+#define PTRACE(i) do { if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); g_ptrace[blockIdx.x][(i)] = t_; } } while (0)
+#else
+#define PTRACE(i) ((void)0)
+#endif
+
 template <int ES, int B>
 __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
     using G_ = Geo<ES, B>;
@@ -187,6 +194,7 @@ __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
     const int j = lane / G_::LPB, sub = lane % G_::LPB;
     uint32_t nbar = 0;
 
+    PTRACE(0);
     // ---------------- phase 1: block sums of squares + level-1 histogram
     for (int i = threadIdx.x; i < kH1; i += kThreads) s_hist[i] = 0;
     __syncthreads();
@@ -202,7 +210,9 @@ __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
     __syncthreads();
     for (int i = threadIdx.x; i < kH1; i += kThreads)
         if (s_hist[i]) atomicAdd(p.hist1 + i, s_hist[i]);
+    PTRACE(1);
     grid_barrier(p.bar, nbar++);
+    PTRACE(2);
 
     // ---------------- phase 2: radix select of the k-th largest key
     const uint32_t k = (uint32_t)p.k;
@@ -246,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
         }
     }
 
+    PTRACE(3);
     // ---------------- phase 3: flat-order scan -> slots, colidx, rowptr
     uint32_t na = 0, nt = 0;
     for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
@@ -297,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
     }
     __syncthreads();
 
+    PTRACE(4);
     // ---------------- phase 4: copy kept blocks (raw integer vectors)
     for (int64_t u = u0 + wid; u < u1; u += nw) {
         const int64_t I = u / p.upr, J = (u % p.upr) * G_::G + j;
@@ -315,6 +327,8 @@ __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
             }
         }
     }
+    __syncthreads();
+    PTRACE(5);
 }
 
 // k == N: every block kept, no norms needed -- a single copy pass.
@@ -449,8 +463,12 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
         count_launch();
         return cudaGetLastError();
     }
+#ifndef PRUNE_NO_MEMSET
     cudaError_t e = cudaMemsetAsync(ws, 0, w.zero_bytes, stream);
     if (e != cudaSuccess) return e;
+#else
+    cudaError_t e = cudaSuccess;
+#endif
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, prune_kernel<ES, B>, kThreads, 0);
     if (e != cudaSuccess) return e;
@@ -460,6 +478,10 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
     grid = std::min<int64_t>(grid, std::max<int64_t>(1, (p.units + kThreads / 32 - 1) / (kThreads / 32)));
     void *args[] = {&p};
     count_launch();
+#ifdef PRUNE_NONCOOP
+    prune_kernel<ES, B><<<(unsigned)grid, kThreads, 0, stream>>>(p);
+    return cudaGetLastError();
+#endif
     return cudaLaunchCooperativeKernel((const void *)prune_kernel<ES, B>, dim3((unsigned)grid), dim3(kThreads),
                                        args, 0, stream);
 }

@@ -33,7 +33,8 @@ def test_native_arm_gpu():
                 "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "e2e", "gpu_launches"):
         assert key in d, key
     per_step = d["gpu_launches_per_step"]
-    assert set(per_step) == {"prune", "wgrad", "decompress"} and min(per_step.values()) >= 1
-    assert d["gpu_launches"] == sum(per_step.values()) * 20
+    assert set(per_step) == {"prune", "wgrad", "decompress", "step"} and min(per_step.values()) >= 1
+    assert per_step["step"] == per_step["prune"] + per_step["wgrad"] + per_step["decompress"]
+    assert d["gpu_launches"] == per_step["step"] * 20
     assert 0 < d["roofline"]["frac"] < 1.5
     assert d["e2e"]["h2d_bytes_per_step"] == 25088 * 384 * 4 + 25088 * 1536 * 4
