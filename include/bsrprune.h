@@ -108,7 +108,12 @@ BSR_API int64_t bsr_keep_count(int64_t nblocks, double keep);
 BSR_API size_t bsr_storage_bytes(int64_t M, int32_t b, int64_t k, int32_t dtype);
 
 /* Device workspace (bytes) bsr_prune / bsr_prune_k need for this shape.
- * 0 on invalid input.  The workspace need not be initialised. */
+ * 0 on invalid input.  The workspace must be zero-filled (cudaMemset) before
+ * its first use and must not be written by anything else between bsr_prune
+ * calls: every call leaves it zero-filled again (its grid barrier and radix
+ * histograms clean themselves), so no per-call clearing is needed.  A
+ * workspace that is not zero-filled makes the kernel trap (BSR launch error)
+ * instead of hanging. */
 BSR_API size_t bsr_prune_workspace_bytes(int64_t M, int64_t K, int32_t b);
 
 /* Device workspace (bytes) bsr_wgrad needs for this shape and precision.  0

@@ -94,12 +94,17 @@ def storage_bytes(M: int, b: int, k: int, dtype=torch.float32) -> int:
 _WS: dict = {}
 
 
-def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
-    """Cached device workspace of at least nbytes (one per device)."""
-    key = (device.type, device.index)
+def workspace(nbytes: int, device: torch.device, kind: str = "wgrad") -> torch.Tensor:
+    """Cached device workspace of at least nbytes, one per (device, kind).
+
+    The prune workspace is zero-filled when allocated and used for nothing else:
+    bsr_prune needs a zero-filled workspace on first use and leaves it that way
+    (include/bsrprune.h)."""
+    key = (device.type, device.index, kind)
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
-        ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        alloc = torch.zeros if kind == "prune" else torch.empty
+        ws = alloc(max(nbytes, 256), dtype=torch.uint8, device=device)
         _WS[key] = ws
     return ws
 
@@ -127,7 +132,7 @@ def prune(X: torch.Tensor, b: int, keep: float | None = None, k: int | None = No
         k = keep_count(N, keep)
     out = out or alloc_bsr(M, K, b, k, X.dtype, X.device)
     ws_bytes = lib.bsr_prune_workspace_bytes(M, K, b)
-    ws = workspace(ws_bytes, X.device)
+    ws = workspace(ws_bytes, X.device, kind="prune")
     cs = out.c_struct()
     _lib.check(lib.bsr_prune_k(X.data_ptr(), M, K, b, k, _dt(X), ctypes.byref(cs), ws.data_ptr(), ws.numel(),
                                _stream(stream)))

@@ -52,8 +52,10 @@ __device__ __forceinline__ void grid_barrier(uint32_t *counter, uint32_t index) 
         __threadfence();
         atomicAdd(counter, 1u);
         const uint32_t target = (index + 1u) * gridDim.x;
+        uint32_t spins = 0;
         while (ld_acquire_gpu(counter) < target) {
             __nanosleep(32);
+            if (++spins > (1u << 26)) __trap();  // workspace not zero-filled / corrupted: fail, do not hang
         }
         __threadfence();
     }

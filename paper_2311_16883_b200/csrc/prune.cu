@@ -281,6 +281,24 @@ __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
         block_excl_scan(pre, s_warp, tot);
         pre = tot;
     }
+    // Self-cleaning workspace: every CTA is past its last read of the barrier counter
+    // and the histograms; the last one to get here zeroes them for the next launch
+    // (so no per-launch memset is needed once the workspace was zero-filled).
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_sel[3] = atomicAdd(p.bar + 32, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_sel[3]) {
+        __threadfence();
+        for (int i = threadIdx.x; i < kH1; i += kThreads) p.hist1[i] = 0;
+        for (int i = threadIdx.x; i < kH2; i += kThreads) p.hist2[i] = 0;
+        for (int i = threadIdx.x; i < kH3; i += kThreads) p.hist3[i] = 0;
+        if (threadIdx.x == 0) {
+            p.bar[0] = 0;
+            p.bar[32] = 0;
+        }
+    }
     uint32_t base_a = (uint32_t)(pre >> 32), base_t = (uint32_t)pre;
     if (blockIdx.x == 0 && threadIdx.x == 0) p.rowptr[0] = 0;
     for (int64_t fb = f0; fb < f1; fb += kThreads) {
@@ -463,12 +481,8 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
         count_launch();
         return cudaGetLastError();
     }
-#ifndef PRUNE_NO_MEMSET
-    cudaError_t e = cudaMemsetAsync(ws, 0, w.zero_bytes, stream);
-    if (e != cudaSuccess) return e;
-#else
+    // (no per-launch memset: the kernel leaves its workspace header zeroed, see above)
     cudaError_t e = cudaSuccess;
-#endif
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, prune_kernel<ES, B>, kThreads, 0);
     if (e != cudaSuccess) return e;

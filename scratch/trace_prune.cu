@@ -15,7 +15,7 @@ int main(int argc, char **argv) {
     float *X, *vals; int *rp, *ci; void *ws;
     cudaMalloc(&X, hX.size() * 4); cudaMemcpy(X, hX.data(), hX.size() * 4, cudaMemcpyHostToDevice);
     cudaMalloc(&vals, (size_t)k * b * b * 4); cudaMalloc(&rp, 4 * (M / b + 1)); cudaMalloc(&ci, 4 * k);
-    auto w = bsrp::prune_ws_layout(N); cudaMalloc(&ws, w.total);
+    auto w = bsrp::prune_ws_layout(N); cudaMalloc(&ws, w.total); cudaMemset(ws, 0, w.total);
     for (int rep = 0; rep < 4; ++rep) {
         cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0);
