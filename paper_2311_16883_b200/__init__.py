@@ -20,7 +20,7 @@ from . import _lib
 from ._lib import BsrError, DT_BF16, DT_F32, PREC
 
 __all__ = ["BSR", "BsrError", "prune", "decompress", "wgrad", "block_sumsq", "num_blocks", "keep_count",
-           "storage_bytes", "workspace", "version"]
+           "storage_bytes", "workspace", "version", "SparseLinear", "sparse_linear"]
 
 _DT = {torch.float32: DT_F32, torch.bfloat16: DT_BF16}
 
@@ -175,3 +175,6 @@ def wgrad(A: BSR, dY: torch.Tensor, prec: str = "fp32", out: torch.Tensor | None
                              ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0,
                              _stream(stream)))
     return out
+
+
+from .sparse_linear import SparseLinear, sparse_linear  # noqa: E402  (uses the functions above)

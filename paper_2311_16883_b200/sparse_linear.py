@@ -1,0 +1,108 @@
+"""Block-sparse linear operator of the paper, built on the hot path.
+
+"The block-sparse linear operator is designed to be a plug-in replacement for
+PyTorch's nn.linear layer with two additional parameters: the level of sparsity,
+and the block size of the sparse structure".  The forward stays
+dense "to ensure an accurate loss computation"; after it, the
+input activation is pruned to its top-k b x b blocks and saved as BSR instead of
+the dense tensor (fig:operator P:L313-321).  In the backward pass
+the weight gradient comes from the BSR while "the input and bias
+gradients do not depend on activations" and are computed densely.
+
+    layer = SparseLinear(384, 1536, sparsity=0.5, block=32)   # keep = 1 - sparsity
+    y = layer(x)            # x: (..., 384) CUDA tensor; rows = prod(leading dims)
+
+Only the dense forward GEMM, dX = dY.W and db = sum(dY) use cuBLAS / PyTorch
+ops (not part of the hot path, BJ "dX stays dense"); block norms, top-k, the
+BSR pack and dW = X_bsr^T . dY run in libbsrprune's sm_100a kernels.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import BSR, prune, wgrad
+
+__all__ = ["SparseLinear", "sparse_linear"]
+
+
+class _SparseLinearFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x2d: torch.Tensor, weight: torch.Tensor, bias, keep: float, block: int, prec: str):
+        y = x2d @ weight.t()
+        if bias is not None:
+            y = y + bias
+        # prune AFTER the dense forward; only the BSR is kept for backward
+        bsr = prune(x2d.detach(), block, keep=keep)
+        ctx.bsr = bsr
+        ctx.prec = prec
+        ctx.has_bias = bias is not None
+        ctx.save_for_backward(weight)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy: torch.Tensor):
+        (weight,) = ctx.saved_tensors
+        bsr: BSR = ctx.bsr
+        dy = dy.contiguous()
+        dx = dy @ weight if ctx.needs_input_grad[0] else None
+        dw = None
+        if ctx.needs_input_grad[1]:
+            dy_w = dy.to(torch.bfloat16) if ctx.prec == "bf16" and dy.dtype != torch.bfloat16 else dy
+            # dW = X_bsr^T . dY is K x N; nn.Linear stores weight as N x K
+            dw = wgrad(bsr, dy_w, prec=ctx.prec).t().to(weight.dtype)
+        db = dy.sum(0) if ctx.has_bias and ctx.needs_input_grad[2] else None
+        ctx.bsr = None
+        return dx, dw, db, None, None, None
+
+
+def _default_prec(dtype: torch.dtype, block: int, out_features: int) -> str:
+    if out_features % 128:
+        return "fp32"  # the tensor-core paths need N % 128 == 0
+    if dtype == torch.bfloat16:
+        return "bf16"
+    return "tf32" if block >= 32 else "fp32"
+
+
+def sparse_linear(x: torch.Tensor, weight: torch.Tensor, bias=None, sparsity: float = 0.5, block: int = 16,
+                  prec: str | None = None) -> torch.Tensor:
+    """Functional form: y = x W^T + b with the input activation saved as top-k BSR."""
+    lead = x.shape[:-1]
+    x2d = x.reshape(-1, x.shape[-1]).contiguous()
+    p = prec or _default_prec(x.dtype, block, weight.shape[0])
+    y = _SparseLinearFn.apply(x2d, weight, bias, 1.0 - float(sparsity), int(block), p)
+    return y.reshape(*lead, weight.shape[0])
+
+
+class SparseLinear(torch.nn.Module):
+    """nn.Linear with two extra parameters, `sparsity` (fraction of blocks pruned,
+    s in the paper) and `block` (b): the saved input activation keeps its
+    round((1 - s) * N) largest-l2-norm b x b blocks."""
+
+    def __init__(self, in_features: int, out_features: int, sparsity: float = 0.5, block: int = 16,
+                 bias: bool = True, prec: str | None = None, device=None, dtype=None):
+        super().__init__()
+        if in_features % block:
+            raise ValueError(f"in_features={in_features} must be a multiple of block={block}")
+        if not 0.0 <= sparsity <= 1.0:
+            raise ValueError("sparsity must be in [0, 1]")
+        self.in_features, self.out_features = in_features, out_features
+        self.sparsity, self.block, self.prec = float(sparsity), int(block), prec
+        kw = dict(device=device, dtype=dtype)
+        self.weight = torch.nn.Parameter(torch.empty(out_features, in_features, **kw))
+        self.bias = torch.nn.Parameter(torch.empty(out_features, **kw)) if bias else None
+        torch.nn.init.kaiming_uniform_(self.weight, a=math.sqrt(5))
+        if self.bias is not None:
+            bound = 1.0 / math.sqrt(in_features)
+            torch.nn.init.uniform_(self.bias, -bound, bound)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if not self.training or not torch.is_grad_enabled():
+            out = x @ self.weight.t()
+            return out + self.bias if self.bias is not None else out
+        return sparse_linear(x, self.weight, self.bias, self.sparsity, self.block, self.prec)
+
+    def extra_repr(self) -> str:
+        return (f"in_features={self.in_features}, out_features={self.out_features}, sparsity={self.sparsity}, "
+                f"block={self.block}, bias={self.bias is not None}")
