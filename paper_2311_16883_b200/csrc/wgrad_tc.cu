@@ -475,6 +475,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t b_lo0 = (uint32_t)smem_desc(sB0, C::B_LBO, C::B_SBO, C::B_LAYOUT);
         long long cyc_wait = 0, cyc_issue = 0, cyc_start = clock64();
         (void)cyc_wait; (void)cyc_issue; (void)cyc_start;
+        // The first n_spec rows are in the sequence whether or not they keep a block:
+        // their dY slabs are requested before the planner has read rowptr/colidx, so
+        // the first HBM round trip overlaps the plan (an empty row costs one slab).
+        const int n_spec = (int)min((int64_t)min(p.stages, first_rows), Ie - Ib);
+        if (is_a)
+            for (int r = 0; r < n_spec; ++r) {
+                mbar_arrive_expect_tx(full + r, (uint32_t)C::A_BYTES);
+                tma_load_3d(&tm_dy, full + r, sA0 + r * C::A_BYTES, 0, (int)(Ib + r) * B, n0 / C::AW);
+            }
         for (int c = 0; c < nchunks; ++c) {
             const int buf = c & 1;
             const int64_t Ic = chunk_start(c);
@@ -485,8 +494,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int r = 0; r < nrow; ++r) {
                 const int4 rr = rows[r];
                 const int cnt = rr.x & 0xFFFF;
-                if (cnt == 0) continue;
+                const bool spec = c == 0 && r < n_spec;
+                if (cnt == 0 && !spec) continue;
                 const int stage = j % p.stages;
+                if (spec && is_a) {  // slab already requested above
+                    ++j;
+                    continue;
+                }
 #ifdef WGRAD_TRACE
                 const long long tw0 = clock64();
 #endif
