@@ -324,8 +324,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nbc = (int)(p.K / B);
     const int J0 = kr * p.kr_blocks;
     const int nbJ = min(p.kr_blocks, nbc - J0);
-    // two MMA warps share the issue work: warp 1 owns block columns [0, jhalf), warp 2 the rest
-    const int jhalf = (nbJ + 1) / 2;
     const int64_t Ib = (int64_t)split * p.nbr / p.nsplit, Ie = (int64_t)(split + 1) * p.nbr / p.nsplit;
     // chunk 0 is short (32 rows) so the first plan is ready early; later chunks are chunk_rows long
     const int first_rows = min(32, p.chunk_rows);
@@ -345,9 +343,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(full + s, 2);   // A producer + B producer
-            mbar_init(empty + s, 2);  // one commit from each MMA warp
+            mbar_init(empty + s, 1);  // the MMA warp's commit
         }
-        mbar_init(accfull, 2);
+        mbar_init(accfull, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(plan_full + i, 1);
             mbar_init(plan_empty + i, 2);  // both producers release a plan chunk
@@ -404,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int jprev = -2, rlen = 0;
                     for (int q = 0; q < cnt; ++q) {
                         const int J = (int)s_col[q0 + q] - J0;
-                        if (J == jprev + 1 && rlen < C::MAX_RUN && J != jhalf) {
+                        if (J == jprev + 1 && rlen < C::MAX_RUN && true) {
                             ++rlen;
                         } else {
                             ++nruns;
@@ -426,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int jprev = -2, rlen = 0, rstart = 0, k = off;
                     for (int q = 0; q < cnt; ++q) {
                         const int J = (int)s_col[q0 + q] - J0;
-                        if (J == jprev + 1 && rlen < C::MAX_RUN && J != jhalf) {
+                        if (J == jprev + 1 && rlen < C::MAX_RUN && true) {
                             ++rlen;
                         } else {
                             if (rlen)
@@ -522,13 +520,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // ready-to-issue runs: TMEM address, B descriptor low word, instruction descriptor
                     const int nruns = rr.x >> 16;
                     uint4 *m = meta + stage * kMetaQuads;
-                    const uint32_t slot_lo = b_lo0 + (uint32_t)((slot0 * C::BLOCK_BYTES) >> 4);
-                    for (int i = 0; i < nruns; ++i) {
+                    for (int i = 0; i < nruns; ++i) {  // compact run word: column | B-ring slot << 10 | length << 22
                         const uint2 run = runs[rr.z + i];
-                        m[1 + i] = make_uint4(tmem + (run.x & 0xFFFFu), slot_lo + (((run.x >> 16) * C::BLOCK_BYTES) >> 4),
-                                              run.y, 0u);
+                        const uint32_t len = ((run.y >> 17) & 0x3Fu) * 8u / (uint32_t)B;
+                        m[1 + i].x = (run.x & 0x3FFu) | ((uint32_t)(slot0 + (int)(run.x >> 16)) << 10) | (len << 22);
                     }
-                    m[0] = make_uint4((uint32_t)nruns, 0u, 0u, 0u);
+                    m[0].x = (uint32_t)nruns;
 #ifdef WGRAD_TRACE
                     const long long tw1 = clock64();
                     cyc_wait += tw1 - tw0;
@@ -566,21 +563,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j >= p.stages) mbar_wait(empty + stage, (uint32_t)((j / p.stages) - 1) & 1u);
         if (!is_a) meta[stage * kMetaQuads] = make_uint4(kEndMarker, 0u, 0u, 0u);
         mbar_arrive(full + stage);
-    } else if (warp == 1 || warp == 2) {
-        // ------------------------------------------------ MMA issuers (whole warps, one elected lane each)
-        // Warp 1 issues the runs in block columns [0, jhalf), warp 2 the rest:
-        // disjoint TMEM columns, so the two issue streams need no ordering; each
-        // commits to every stage's `empty` barrier (count 2) and to `accfull`.
-        // Every lane reads the same ready-to-issue run words; redux.sync makes them
-        // warp-uniform, so each tcgen05.mma is one predicated UTCHMMA.
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer (whole warp, one elected lane issues)
+        // Lane i loads word i of the stage's metadata (header + runs) with ONE shared
+        // load; each run word becomes warp-uniform with a single masked redux, and
+        // the descriptors are built from it with uniform arithmetic, so every
+        // tcgen05.mma is one predicated UTCHMMA.
         const uint64_t a_desc0 = smem_desc(smem_u32(ringA), C::A_LBO, C::A_SBO, C::A_LAYOUT);
         const uint32_t a_lo0 = (uint32_t)a_desc0, a_hi = (uint32_t)(a_desc0 >> 32);
-        const uint32_t b_hi = (uint32_t)(smem_desc(smem_u32(ringB), C::B_LBO, C::B_SBO, C::B_LAYOUT) >> 32);
-        const uint32_t col_split = tmem + (uint32_t)(jhalf * B);
+        const uint64_t b_desc0 = smem_desc(smem_u32(ringB), C::B_LBO, C::B_SBO, C::B_LAYOUT);
+        const uint32_t b_lo0 = (uint32_t)b_desc0, b_hi = (uint32_t)(b_desc0 >> 32);
+        const uint32_t idesc0 = instr_desc<KIND>(0u);
         int stage = 0;
         uint32_t phase = 0;
-        long long mw = 0, mi = 0, m_start = clock64();
-        (void)mw; (void)mi; (void)m_start;
+        long long mw = 0, mi = 0, m_start = clock64(), nrow_m = 0;
+        (void)mw; (void)mi; (void)m_start; (void)nrow_m;
         for (;;) {
 #ifdef WGRAD_TRACE
             const long long t0m = clock64();
@@ -590,28 +587,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef WGRAD_TRACE
             const long long t1m = clock64();
             mw += t1m - t0m;
+            ++nrow_m;
 #endif
-            const uint4 *m = meta + stage * kMetaQuads;
-            const uint32_t nruns = __reduce_or_sync(0xffffffffu, m[0].x);
+            const uint32_t m_addr = smem_u32(meta + stage * kMetaQuads);
+            uint32_t wl;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wl) : "r"(m_addr + lane * 16u));
+            const uint32_t nruns = __reduce_or_sync(0xffffffffu, lane == 0 ? wl : 0u);
             if (nruns == kEndMarker) break;
             const uint32_t a_lo = a_lo0 + (uint32_t)((stage * C::A_BYTES) >> 4);
             for (uint32_t i = 0; i < nruns; ++i) {
-                const uint4 w = m[1 + i];
-                const uint32_t d = __reduce_or_sync(0xffffffffu, w.x);
-                if ((d < col_split) != (warp == 1)) continue;
-                const uint32_t b_lo = __reduce_or_sync(0xffffffffu, w.y);
-                const uint32_t idesc = __reduce_or_sync(0xffffffffu, w.z);
+                uint32_t w = wl;
+                if (i + 1 >= 32) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(m_addr + (i + 1) * 16u));
+                const uint32_t rw = __reduce_or_sync(0xffffffffu, (i + 1 >= 32 || lane == i + 1) ? w : 0u);
+                const uint32_t d = tmem + (rw & 0x3FFu);
+                const uint32_t b_lo = b_lo0 + ((rw >> 10) & 0xFFFu) * (uint32_t)(C::BLOCK_BYTES >> 4);
+                const uint32_t idesc = idesc0 | ((((rw >> 22) & 0x3Fu) * (uint32_t)B >> 3) << 17);
 #pragma unroll
                 for (int s = 0; s < B / C::UK; ++s)
-                    if (!(WGRAD_TRACE_MODE & 2))
-                        tc_mma_elect<KIND>(d, a_lo + ((s * C::A_KSTEP) >> 4), a_hi, b_lo + ((s * C::B_KSTEP) >> 4), b_hi,
-                                           idesc);
+                    tc_mma_elect<KIND>(d, a_lo + ((s * C::A_KSTEP) >> 4), a_hi, b_lo + ((s * C::B_KSTEP) >> 4), b_hi,
+                                       idesc);
             }
             __syncwarp();
-            if (lane == 0) {
-                if (WGRAD_TRACE_MODE & 4) mbar_arrive(empty + stage); else
-                tc_commit(empty + stage);  // frees the stage (and its B slots) once these MMAs complete
-            }
+            if (lane == 0) tc_commit(empty + stage);  // frees the stage (and its B slots) once these MMAs complete
             __syncwarp();
 #ifdef WGRAD_TRACE
             mi += clock64() - t1m;
@@ -620,9 +617,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 #ifdef WGRAD_TRACE
         if (lane == 0) {
-            g_trace[blockIdx.x][218 + 3 * (warp - 1)] = (unsigned long long)mw;
-            g_trace[blockIdx.x][219 + 3 * (warp - 1)] = (unsigned long long)mi;
-            g_trace[blockIdx.x][220 + 3 * (warp - 1)] = (unsigned long long)(clock64() - m_start);
+            g_trace[blockIdx.x][218] = (unsigned long long)mw;
+            g_trace[blockIdx.x][219] = (unsigned long long)mi;
+            g_trace[blockIdx.x][220] = (unsigned long long)(clock64() - m_start);
         }
 #endif
         if (lane == 0) tc_commit(accfull);
