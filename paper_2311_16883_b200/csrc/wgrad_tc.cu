@@ -7,27 +7,32 @@
 // Orientation: the MMA computes D = dW^T tile-wise,
 //   D[n][kcol] (TMEM: 128 lanes = 128 columns n of dY, one TMEM column per
 //   kcol of X) += A[n][r] * B[r][kcol]
-// with A = the b x 128 slab of dY of block row I (MN-major: n contiguous,
-// exactly dY's row-major layout) and B = the stored X blocks of that block
-// row (MN-major: kcol contiguous, exactly the BSR block layout).  Every kept
-// block becomes b/UMMA_K MMAs of shape 128 x b x UMMA_K into its own TMEM
-// column range, so pruned blocks cost nothing; runs of adjacent kept blocks
-// (consecutive in BSR storage, hence consecutive in shared memory) merge into
-// one MMA with N = run * b <= 256.  Block rows without a kept block in the
-// CTA's column range are never read.
+// with A = the b x 128 slab of dY of block row I and B = the stored X blocks of
+// that block row (MN-major: kcol contiguous, exactly the BSR block layout,
+// staged in shared memory by TMA).  Every kept block becomes b/UMMA_K MMAs of
+// shape 128 x b x UMMA_K into its own TMEM column range, so pruned blocks cost
+// nothing; runs of adjacent kept blocks (consecutive in BSR storage, hence
+// consecutive in shared memory) merge into one MMA with N = run * b <= 256.
+// Block rows without a kept block in the CTA's column range are never read.
 //
-// CTA = (128-column tile of dY) x (range of <= 512 kcols: TMEM columns) x
-// (range of block rows: split-K).  Warp roles: warp 0 = TMA producer, warp 1 =
-// MMA issuer, warp 2 = TMEM allocator, warp 3 = block-row metadata prefetcher
-// (rowptr/colidx chunks into shared memory, double-buffered), warps 4-7 =
-// epilogue (tcgen05.ld -> fp32 stores of this split's partial tile).
-// Shared memory holds an A ring (one b x 128 dY slab per block row, loaded with
-// ONE 3-D TMA) and a B ring of block slots (a row's kept blocks are consecutive
-// in BSR storage and land in consecutive slots, loaded G blocks per 4-D TMA),
-// swizzled by TMA exactly as the UMMA descriptors expect.  The producer turns
-// each row into a list of MMA runs (consecutive block columns, N <= 256) so the
-// per-row instruction count of both single-thread roles stays small -- the
-// per-row issue cost, not HBM, bounds a naive version of this kernel.
+// A lives in TENSOR memory (the `.kind [d], [a_tmem], b_desc` form): the slab is
+// shared by every run of its row, and an MMA that reads A from shared memory
+// pays 4 KB of shared-memory bandwidth per instruction (measured floor 32 + N/4
+// cycles per MMA, scratch/umma_mw.cu) -- more than the math itself for the
+// short runs of a pruned row (N/2 cycles).  Each slab is loaded by ONE 2-D
+// TMA into a shared-memory A ring (per-thread global loads top out near half
+// the HBM bandwidth for this access pattern, scratch/ldg_stream.cu), then warps
+// 4-7 move it shared -> registers -> tcgen05.st into one of NA TMEM A buffers;
+// with A in TMEM the MMAs only read their B blocks from shared memory.
+//
+// CTA = (128-column tile of dY) x (range of kcols: TMEM columns) x (range of
+// block rows: split-K).  Warp roles: warp 0 = B producer (TMA), warp 1 = MMA
+// issuer for the lower half of the accumulator columns, warp 2 = TMEM allocator
+// then MMA issuer for the upper half, warp 3 = block-row planner (rowptr/colidx
+// chunks -> per-row MMA runs and B-ring slots, double-buffered), warps 4-7 = A
+// movers for the even rows of the sequence during the main loop, then the
+// epilogue (tcgen05.ld -> TMA bulk stores of this split's partial tile), warp 8 =
+// A producer (dY slab TMAs), warps 9-12 = A movers for the odd rows.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -42,21 +47,21 @@
 namespace bsrp {
 namespace tc {
 
-constexpr int kThreads = 256;
-// per stage (uint4 units), written by the B producer: [0].x = number of MMA runs
-// (kEndMarker = no more rows); [1..] = one MMA run each, ready to issue:
-// x = TMEM address of its first column, y = low word of the B descriptor (k-step
-// 0), z = UMMA instruction descriptor (encodes N = run length * b)
-constexpr int kMetaQuads = 34;
-constexpr uint32_t kEndMarker = 0xFFFFu;
-constexpr int kStageExtra = kMetaQuads * 16 + 4 + 16;  // meta + slot-use word + full/empty mbarriers
+constexpr int kThreads = 416;  // 13 warps (roles below)
+constexpr int kStages = 24;        // rows whose B blocks may be resident at once
+constexpr int kMaxA = 4;           // TMEM A buffers (rows in flight between the A movers and the MMA warps)
+constexpr int kMaxSA = 8;          // shared-memory A ring stages (dY slabs in flight from HBM)
+constexpr int kIssuers = 2;        // MMA-issuing warps (1 and 2), each owning half of the accumulator columns
 constexpr int kSmemBudget = 227 * 1024;
-constexpr int kColCap = 1024;      // kept blocks of one metadata chunk (colidx staged in smem; one run each at most)
-constexpr int kRowCap = 255;       // block rows of one metadata chunk
-// alignment slack + barriers/TMEM slot + rowptr/colidx scratch + two row-plan buffers
-// (16-byte row records + 8-byte run records)
-constexpr int kFixedSmem = 1024 + 1024 + 4 * (kRowCap + 1) + 2 * kColCap + 2 * (16 * kRowCap + 8 * kColCap);
+constexpr int kColCap = 1536;      // stored blocks of one metadata chunk (colidx staged in smem; one run each at most)
+constexpr int kStepCap = 64;       // steps of one metadata chunk
+constexpr int kMaxR = 4;           // block rows per step (b = 16)
+// alignment slack + barriers/TMEM slot + slot-use words + two plan buffers (16-byte
+// step records, 8-byte block-row records, 4-byte run words) + rowptr/colidx scratch
+constexpr int kFixedSmem = 1024 + 1024 + kStages * 4 + 2 * (16 * kStepCap + 8 * kStepCap * kMaxR + 4 * kColCap) +
+                           4 * (kStepCap * kMaxR + 1) + 2 * kColCap;
 constexpr int kSplitSMs = 148;     // bound on split-K CTAs used to size the workspace (B200: 148 SMs)
+constexpr int kEpiBytes = 2 * 32 * 128 * 4;  // epilogue staging (two 32 x 128 fp32 tiles, reuses the B ring)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -90,14 +95,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         if (++spins > (1u << 26)) __trap();
     }
 }
-
-__device__ __forceinline__ void tma_load_3d(const CUtensorMap *tm, uint64_t *bar, uint32_t dst, int x, int y, int z) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-            dst),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-        : "memory");
+// Slow wait for warps that idle for a long stretch: back off so they do not
+// steal issue slots from the producer and MMA warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) __nanosleep(256);
 }
+
 __device__ __forceinline__ void tma_load_4d(const CUtensorMap *tm, uint64_t *bar, uint32_t dst, int x, int y, int z,
                                             int w) {
     asm volatile(
@@ -115,84 +118,71 @@ __device__ __forceinline__ void tc_commit(uint64_t *bar) {
                  : "memory");
 }
 
-template <int KIND>
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                       uint32_t accumulate) {
-    if constexpr (KIND == 1) {
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-    } else {
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-    }
-}
-
-// All B/UK k-steps of one MMA run in a single asm block: descriptors advance by
-// constant byte offsets (>> 4) inside PTX, so the issuing thread moves the base
-// descriptors into uniform registers once per run instead of once per MMA.
-#define BSRP_MMA2(KS)                                                                                    \
-    asm volatile("{\n.reg .b64 a1, b1;\n"                                                                 \
-                 "add.s64 a1, %1, %4;\nadd.s64 b1, %2, %5;\n"                                             \
-                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], %1, %2, %3, 1;\n"                          \
-                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], a1, b1, %3, 1;\n}\n" ::"r"(d_tmem),         \
-                 "l"(a_desc), "l"(b_desc), "r"(idesc), "n"(AK), "n"(BK))
-#define BSRP_MMA4(KS)                                                                                    \
-    asm volatile("{\n.reg .b64 a1, b1, a2, b2, a3, b3;\n"                                                 \
-                 "add.s64 a1, %1, %4;\nadd.s64 b1, %2, %5;\n"                                             \
-                 "add.s64 a2, %1, %6;\nadd.s64 b2, %2, %7;\n"                                             \
-                 "add.s64 a3, %1, %8;\nadd.s64 b3, %2, %9;\n"                                             \
-                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], %1, %2, %3, 1;\n"                          \
-                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], a1, b1, %3, 1;\n"                          \
-                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], a2, b2, %3, 1;\n"                          \
-                 "tcgen05.mma.cta_group::1.kind::" KS " [%0], a3, b3, %3, 1;\n}\n" ::"r"(d_tmem),         \
-                 "l"(a_desc), "l"(b_desc), "r"(idesc), "n"(AK), "n"(BK), "n"(2 * AK), "n"(2 * BK),         \
-                 "n"(3 * AK), "n"(3 * BK))
-template <int KIND, int NSTEP, int AK, int BK>
-__device__ __forceinline__ void tc_mma_run(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc) {
-    if constexpr (NSTEP == 1) {
-        tc_mma<KIND>(d_tmem, a_desc, b_desc, idesc, 1u);
-    } else if constexpr (NSTEP == 2) {
-        if constexpr (KIND == 1) BSRP_MMA2("f16"); else BSRP_MMA2("tf32");
-    } else if constexpr (NSTEP == 4) {
-        if constexpr (KIND == 1) BSRP_MMA4("f16"); else BSRP_MMA4("tf32");
-    } else {
-        static_assert(NSTEP % 4 == 0, "k steps per block");
-#pragma unroll
-        for (int s = 0; s < NSTEP; s += 4)
-            tc_mma_run<KIND, 4, AK, BK>(d_tmem, a_desc + (uint64_t)(s * AK), b_desc + (uint64_t)(s * BK), idesc);
-    }
-}
-#undef BSRP_MMA2
-#undef BSRP_MMA4
-
-// tcgen05.mma issued by one elected lane of a converged warp; the 64-bit
-// descriptors are assembled from 32-bit halves inside PTX.  Every operand is
+// tcgen05.mma with A in TMEM, issued by one elected lane of a converged warp;
+// the B descriptor is assembled from 32-bit halves inside PTX.  Every operand is
 // warp-uniform, so ptxas keeps them in uniform registers.
 template <int KIND>
-__device__ __forceinline__ void tc_mma_elect(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
-                                             uint32_t b_hi, uint32_t idesc) {
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t b_hi,
+                                          uint32_t idesc) {
     if constexpr (KIND == 1) {
         asm volatile(
-            "{\n.reg .pred p;\n.reg .b64 a, b;\nmov.b64 a, {%1, %2};\nmov.b64 b, {%3, %4};\n"
+            "{\n.reg .pred p;\n.reg .b64 b;\nmov.b64 b, {%2, %3};\n"
             "elect.sync _|p, 0xffffffff;\n"
-            "@p tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, 1;\n}\n" ::"r"(d_tmem),
-            "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc));
+            "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], b, %4, 1;\n}\n" ::"r"(d_tmem),
+            "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc));
     } else {
         asm volatile(
-            "{\n.reg .pred p;\n.reg .b64 a, b;\nmov.b64 a, {%1, %2};\nmov.b64 b, {%3, %4};\n"
+            "{\n.reg .pred p;\n.reg .b64 b;\nmov.b64 b, {%2, %3};\n"
             "elect.sync _|p, 0xffffffff;\n"
-            "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], a, b, %5, 1;\n}\n" ::"r"(d_tmem),
-            "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc));
+            "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], b, %4, 1;\n}\n" ::"r"(d_tmem),
+            "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc));
     }
 }
+
+// All NSTEP k-steps of one MMA run (A in TMEM) in ONE asm block: one elect, the
+// operands enter once, and the per-step A column / B address offsets are added
+// inside PTX, so the issuing warp spends ~2 instructions per MMA.
+#define BSRP_TS_HEAD "{\n.reg .pred p;\n.reg .b32 a<8>, bl<8>;\n.reg .b64 b<8>;\nelect.sync _|p, 0xffffffff;\n"
+#define BSRP_TS_STEP(KS, S)                                                                             \
+    "add.u32 a" #S ", %1, " #S "*%5;\nadd.u32 bl" #S ", %2, " #S "*%6;\nmov.b64 b" #S ", {bl" #S ", %3};\n" \
+    "@p tcgen05.mma.cta_group::1.kind::" KS " [%0], [a" #S "], b" #S ", %4, 1;\n"
+#define BSRP_TS_ARGS                                                                                      \
+    ::"r"(d_tmem), "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc), "n"(AKC), "n"(BK16)
+template <int KIND, int NSTEP, int AKC, int BK16>
+__device__ __forceinline__ void tc_mma_ts_run(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t b_hi,
+                                              uint32_t idesc) {
+    if constexpr (NSTEP == 1) {
+        if constexpr (KIND == 1) asm volatile(BSRP_TS_HEAD BSRP_TS_STEP("f16", 0) "}\n" BSRP_TS_ARGS);
+        else asm volatile(BSRP_TS_HEAD BSRP_TS_STEP("tf32", 0) "}\n" BSRP_TS_ARGS);
+    } else if constexpr (NSTEP == 2) {
+        if constexpr (KIND == 1) asm volatile(BSRP_TS_HEAD BSRP_TS_STEP("f16", 0) BSRP_TS_STEP("f16", 1) "}\n" BSRP_TS_ARGS);
+        else asm volatile(BSRP_TS_HEAD BSRP_TS_STEP("tf32", 0) BSRP_TS_STEP("tf32", 1) "}\n" BSRP_TS_ARGS);
+    } else if constexpr (NSTEP == 4) {
+        if constexpr (KIND == 1)
+            asm volatile(BSRP_TS_HEAD BSRP_TS_STEP("f16", 0) BSRP_TS_STEP("f16", 1) BSRP_TS_STEP("f16", 2)
+                             BSRP_TS_STEP("f16", 3) "}\n" BSRP_TS_ARGS);
+        else
+            asm volatile(BSRP_TS_HEAD BSRP_TS_STEP("tf32", 0) BSRP_TS_STEP("tf32", 1) BSRP_TS_STEP("tf32", 2)
+                             BSRP_TS_STEP("tf32", 3) "}\n" BSRP_TS_ARGS);
+    } else {
+        static_assert(NSTEP == 8, "k steps per block");
+        if constexpr (KIND == 1)
+            asm volatile(BSRP_TS_HEAD BSRP_TS_STEP("f16", 0) BSRP_TS_STEP("f16", 1) BSRP_TS_STEP("f16", 2)
+                             BSRP_TS_STEP("f16", 3) BSRP_TS_STEP("f16", 4) BSRP_TS_STEP("f16", 5)
+                                 BSRP_TS_STEP("f16", 6) BSRP_TS_STEP("f16", 7) "}\n" BSRP_TS_ARGS);
+        else
+            asm volatile(BSRP_TS_HEAD BSRP_TS_STEP("tf32", 0) BSRP_TS_STEP("tf32", 1) BSRP_TS_STEP("tf32", 2)
+                             BSRP_TS_STEP("tf32", 3) BSRP_TS_STEP("tf32", 4) BSRP_TS_STEP("tf32", 5)
+                                 BSRP_TS_STEP("tf32", 6) BSRP_TS_STEP("tf32", 7) "}\n" BSRP_TS_ARGS);
+    }
+}
+#undef BSRP_TS_HEAD
+#undef BSRP_TS_STEP
+#undef BSRP_TS_ARGS
 
 // UMMA shared-memory matrix descriptor (sm_100): start, leading-byte offset
 // (stride between MN atoms for swizzled MN-major), stride-byte offset (between
-// 8-row K groups), version 1, swizzle layout type.
+// K groups), version 1, swizzle layout type.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -204,11 +194,11 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // Instruction descriptor: fp32 accumulate, A/B format (1 = bf16, 2 = tf32),
-// both operands MN-major, M = 128, N = n.
+// A K-major (A in TMEM), B MN-major, M = 128, N = n.
 template <int KIND>
-__device__ __forceinline__ uint32_t instr_desc(uint32_t n) {
+__host__ __device__ __forceinline__ uint32_t instr_desc(uint32_t n) {
     constexpr uint32_t fmt = KIND == 1 ? 1u : 2u;
-    return (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 15) | (1u << 16) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+    return (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) | ((n >> 3) << 17) | ((128u >> 4) << 24);
 }
 
 #define TMEM_LD16(taddr, v)                                                                                     \
@@ -225,25 +215,31 @@ __device__ __forceinline__ void tmem_st16_zero(uint32_t taddr) {
         "r"(z)
         : "memory");
 }
+// 8 consecutive TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t *v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
 
 struct Params {
     const int32_t *rowptr, *colidx;
+    const uint8_t *values;
     float *dW, *ws;
     int64_t nbr, N, K;
     int nkr, nsplit, kr_blocks;  // kcol range = kr_blocks blocks
-    int stages, nbslots, mode;   // A-ring stages, B-ring block slots; mode: 0 store, 1 load-add-store, 3 partial -> ws[split]
-    int chunk_rows;              // block rows of one metadata chunk (rowptr + colidx staged in smem)
-    uint32_t tmem_cols;
+    int nbslots, na, mode;       // B-ring block slots, TMEM A buffers; mode: 0 store, 1 reduce-add, 3 partial -> ws[split]
+    int chunk_steps;             // steps of one metadata chunk (rowptr + colidx staged in smem)
+    int sa;                      // shared-memory A ring stages
+    uint32_t a_col0;             // first TMEM column of the A buffers
 };
 
 template <int KIND, int B>
 struct Cfg {
     static constexpr int ES = KIND == 1 ? 2 : 4;
     static constexpr int UK = KIND == 1 ? 16 : 8;           // MMA K per instruction
-    static constexpr int AW = 128 / ES;                     // dY columns per 128-byte swizzle atom
-    static constexpr int A_ATOMS = 128 / AW;                // atoms along M = 128
-    static constexpr int A_BYTES = B * 128 * ES;            // b rows x 128 columns
-    static constexpr int A_LBO = B * 128;                   // bytes between M atoms
+    static constexpr int A_COLS = B * ES / 4;               // TMEM columns of one block row's slab (32-bit, K packed)
+    static constexpr int A_KCOLS = UK * ES / 4;             // TMEM columns per MMA K step (8)
     static constexpr int BW = (B * ES < 128) ? B * ES : 128;  // block row bytes per swizzle atom
     static constexpr int B_ATOMS = B * ES / BW;
     static constexpr int BLOCK_BYTES = B * B * ES;
@@ -254,15 +250,28 @@ struct Cfg {
     // plain SW32/64/128 layouts with K groups of 8 rows.
     static constexpr bool TF32 = KIND == 0;
     static constexpr int KGROUP = TF32 ? 4 : 8;             // K rows per swizzle group
-    static constexpr int A_SBO = KGROUP * 128;              // bytes between K groups of A
-    static constexpr uint32_t A_LAYOUT = TF32 ? 1u : 2u;
-    static constexpr int A_KSTEP = UK * 128;                // bytes per MMA K step in A
     static constexpr int B_SBO = KGROUP * BW;               // bytes between K groups of B
     static constexpr int B_KSTEP = UK * BW;                 // bytes per MMA K step in B
     static constexpr uint32_t B_LAYOUT = TF32 ? 1u : BW == 128 ? 2u : BW == 64 ? 4u : 6u;  // SW128_32B / SW128 / SW64 / SW32
     static_assert(!TF32 || BW == 128, "tf32 MN-major operands need 128-byte block rows (b >= 32)");
     static constexpr int MAX_RUN = 256 / B;                 // blocks per MMA (N <= 256)
+#ifdef WGRAD_G
+    static constexpr int G = WGRAD_G;  // dev sweeps only
+#else
     static constexpr int G = BLOCK_BYTES >= 8192 ? 1 : BLOCK_BYTES >= 2048 ? 4 : 8;  // blocks per B TMA
+#endif
+    // One pipeline step = R consecutive block rows (64 dY rows): one dY slab TMA,
+    // one TMEM A buffer, one trip through every barrier.  The per-step
+    // synchronisation (each mbarrier wait costs ~100 cycles even when the phase
+    // has completed) is paid once per 64 rows instead of once per block row.
+#ifdef WGRAD_R
+    static constexpr int R = WGRAD_R;  // dev sweeps only
+#else
+    static constexpr int R = B >= 64 ? 1 : 64 / B;
+#endif
+    static constexpr int SROWS = R * B;                     // dY rows per step
+    static constexpr int A_STEP = R * A_COLS;               // TMEM columns of one step's A buffer
+    static constexpr int SLAB = SROWS * 128 * ES;           // one dY slab (SROWS rows x 128 columns, row-major)
 };
 
 #ifdef WGRAD_TRACE
@@ -273,17 +282,55 @@ __device__ __forceinline__ unsigned long long gtime() {
     return t;
 }
 #define TRACE(slot) (g_trace[blockIdx.x][(slot)] = gtime())
+__device__ long long g_lat[160][4][64];  // [cta][B issue, B ready, A issue, A ready][step j < 64]
+#define TLAT(kind, j) do { if ((j) < 64) g_lat[blockIdx.x][kind][(j)] = clock64(); } while (0)
+#define TCLK(v) const long long v = clock64()
+#define TADD(acc, v) (acc += clock64() - (v))
+#define TSET(slot, val) (g_trace[blockIdx.x][(slot)] = (unsigned long long)(val))
 #else
 #define TRACE(slot) ((void)0)
+#define TCLK(v) ((void)0)
+#define TADD(acc, v) ((void)0)
+#define TSET(slot, val) ((void)0)
+#define TLAT(kind, j) ((void)0)
 #endif
 #ifndef WGRAD_TRACE_MODE
-#define WGRAD_TRACE_MODE 0  // dev experiments only: 1 = no loads, 2 = no MMAs
+#define WGRAD_TRACE_MODE 0  // dev experiments only: bit 0 = no MMAs, bit 1 = no B loads, bit 2 = no A loads
 #endif
 
-// Slow wait for warps that idle for the whole main loop (epilogue): back off so
-// they do not steal issue slots from the producer and MMA warps.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) __nanosleep(256);
+// This thread's dY column of the step's slab in shared memory (row-major, 128
+// columns per row): SROWS values; consecutive lanes read consecutive elements
+// (conflict-free).
+template <int KIND, int N_>
+__device__ __forceinline__ void lds_slab(uint32_t (&v)[N_], uint32_t saddr) {
+#pragma unroll
+    for (int k = 0; k < N_; ++k) {
+        if constexpr (KIND == 1) {
+            unsigned short h;
+            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(saddr + k * 256));
+            v[k] = h;
+        } else {
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v[k]) : "r"(saddr + k * 512));
+        }
+    }
+}
+
+// The slab into TMEM columns [taddr, taddr + N_ * ES / 4) of this thread's lane
+// (K-major A: column j holds K element j, or K elements 2j, 2j+1 for bf16).
+template <int KIND, int N_>
+__device__ __forceinline__ void store_slab(uint32_t taddr, const uint32_t (&v)[N_]) {
+    if constexpr (KIND == 1) {
+#pragma unroll
+        for (int c = 0; c < N_ / 2; c += 8) {
+            uint32_t w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = v[2 * (c + i)] | (v[2 * (c + i) + 1] << 16);
+            tmem_st8(taddr + c, w);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < N_; c += 8) tmem_st8(taddr + c, v + c);
+    }
 }
 
 template <int KIND, int B>
@@ -291,25 +338,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_val,
                     const __grid_constant__ CUtensorMap tm_dw, const __grid_constant__ CUtensorMap tm_ws, Params p) {
     using C = Cfg<KIND, B>;
-    // shared memory: [A ring: stages x A_BYTES][B ring: nbslots x BLOCK_BYTES][meta: stages x kMetaPairs]
-    //   [slot use: stages][mbarriers][TMEM slot][rowptr scratch][colidx scratch][2 x row records][2 x run records]
+    constexpr int R = C::R;
+    // shared memory: [A ring: sa x SLAB][B ring: nbslots x BLOCK_BYTES][slot use: kStages][mbarriers]
+    //   [TMEM slot][step records][sub-row records][run words][rowptr scratch][colidx scratch]
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *ringA = smem;
-    uint8_t *ringB = ringA + (size_t)p.stages * C::A_BYTES;
-    uint4 *meta = reinterpret_cast<uint4 *>(ringB + (size_t)p.nbslots * C::BLOCK_BYTES);
-    uint32_t *s_used = reinterpret_cast<uint32_t *>(meta + p.stages * kMetaQuads);
-    uint64_t *full = reinterpret_cast<uint64_t *>(s_used + ((p.stages + 1) & ~1));
-    uint64_t *empty = full + p.stages;
-    uint64_t *accfull = empty + p.stages;
+    uint8_t *ringB = ringA + (size_t)p.sa * C::SLAB;
+    uint32_t *s_used = reinterpret_cast<uint32_t *>(ringB + (size_t)p.nbslots * C::BLOCK_BYTES);
+    uint64_t *full = reinterpret_cast<uint64_t *>(s_used + kStages);
+    uint64_t *empty = full + kStages;
+    uint64_t *afull = empty + kStages;     // [kMaxA]
+    uint64_t *aempty = afull + kMaxA;      // [kMaxA]
+    uint64_t *sfull = aempty + kMaxA;      // [kMaxSA] A ring: slab landed (TMA bytes)
+    uint64_t *sempty = sfull + kMaxSA;     // [kMaxSA] A ring: slab read by the four A movers
+    uint64_t *accfull = sempty + kMaxSA;
     uint64_t *plan_full = accfull + 1;     // [2]
     uint64_t *plan_empty = plan_full + 2;  // [2]
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(plan_empty + 2);
-    int4 *s_rows = reinterpret_cast<int4 *>((reinterpret_cast<uintptr_t>(s_tmem + 4) + 15) & ~uintptr_t(15));
-    // s_rows [2][kRowCap]: cnt | nruns << 16, B-ring need, run offset, first value index
-    uint2 *s_runs = reinterpret_cast<uint2 *>(s_rows + 2 * kRowCap);      // [2][kColCap]
-    int32_t *s_rp = reinterpret_cast<int32_t *>(s_runs + 2 * kColCap);   // [kRowCap + 1]
-    uint16_t *s_col = reinterpret_cast<uint16_t *>(s_rp + kRowCap + 1);  // [kColCap]
+    // s_steps [2][kStepCap] (one per step of the chunk): x = MMA runs, y = B-ring
+    //   slots used (needs + wasted tail slots) | in-sequence << 30, z = first run
+    //   word, w = B bytes
+    // s_sub [2][kStepCap * R] (one per block row): x = first value index, y = first
+    //   B-ring slot | blocks to load (G rounded) << 16
+    // s_runs [2][kColCap]: one ready-to-issue word per MMA run: TMEM column |
+    //   B-ring slot << 10 | run length (blocks) << 22 | block row within the step << 28
+    int4 *s_steps = reinterpret_cast<int4 *>((reinterpret_cast<uintptr_t>(s_tmem + 4) + 15) & ~uintptr_t(15));
+    uint2 *s_sub = reinterpret_cast<uint2 *>(s_steps + 2 * kStepCap);
+    uint32_t *s_runs = reinterpret_cast<uint32_t *>(s_sub + 2 * kStepCap * R);
+    int32_t *s_rp = reinterpret_cast<int32_t *>(s_runs + 2 * kColCap);  // [kStepCap * R + 1]
+    uint16_t *s_col = reinterpret_cast<uint16_t *>(s_rp + kStepCap * R + 1);  // [kColCap]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // Consecutive CTAs take consecutive 128-column tiles of the same block rows,
@@ -324,38 +382,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nbc = (int)(p.K / B);
     const int J0 = kr * p.kr_blocks;
     const int nbJ = min(p.kr_blocks, nbc - J0);
-    const int64_t Ib = (int64_t)split * p.nbr / p.nsplit, Ie = (int64_t)(split + 1) * p.nbr / p.nsplit;
-    // chunk 0 is short (32 rows) so the first plan is ready early; later chunks are chunk_rows long
-    const int first_rows = min(32, p.chunk_rows);
-    const int64_t nrows_cta = Ie - Ib;
-    const int nchunks = nrows_cta <= first_rows ? (nrows_cta > 0 ? 1 : 0)
-                                                : 1 + (int)((nrows_cta - first_rows + p.chunk_rows - 1) / p.chunk_rows);
-    auto chunk_start = [&](int c) -> int64_t { return c == 0 ? Ib : Ib + first_rows + (int64_t)(c - 1) * p.chunk_rows; };
-    auto chunk_len = [&](int c) -> int {
-        return (int)min((int64_t)(c == 0 ? first_rows : p.chunk_rows), Ie - chunk_start(c));
+    const int64_t nst = (p.nbr + R - 1) / R;  // steps (the last one may hold fewer than R block rows)
+    const int64_t Sb = (int64_t)split * nst / p.nsplit, Se = (int64_t)(split + 1) * nst / p.nsplit;
+    // chunk 0 is short (8 steps) so the first plan is ready early; later chunks are chunk_steps long
+    const int first_steps = min(8, p.chunk_steps);
+    const int64_t nsteps_cta = Se - Sb;
+    const int nchunks = nsteps_cta <= first_steps ? (nsteps_cta > 0 ? 1 : 0)
+                                                  : 1 + (int)((nsteps_cta - first_steps + p.chunk_steps - 1) / p.chunk_steps);
+    auto chunk_start = [&](int c) -> int64_t {
+        return c == 0 ? Sb : Sb + first_steps + (int64_t)(c - 1) * p.chunk_steps;
     };
+    auto chunk_len = [&](int c) -> int {
+        return (int)min((int64_t)(c == 0 ? first_steps : p.chunk_steps), Se - chunk_start(c));
+    };
+    // The first n_spec steps are in the sequence whether or not they keep a block:
+    // their dY slabs are requested before the planner has read rowptr/colidx, so
+    // the first HBM round trip overlaps the plan (an empty step costs one slab).
+    const int n_spec = (int)min((int64_t)min(p.sa, first_steps), nsteps_cta);
+    // MMA warp 1 owns accumulator blocks [0, jhalf), warp 2 blocks [jhalf, nbJ)
+    const int jhalf = (nbJ + 1) / 2;
     if (threadIdx.x == 0) TRACE(0);
 
-    if (warp == 0 && lane == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_dy)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_val)) : "memory");
-    }
+    if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_val)) : "memory");
+    if (warp == 8 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_dy)) : "memory");
     if (warp == 1 && lane == 0) {
-        for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full + s, 2);   // A producer + B producer
-            mbar_init(empty + s, 1);  // the MMA warp's commit
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(full + s, 1);          // the B producer (+ TMA bytes)
+            mbar_init(empty + s, kIssuers);  // the MMA warps' commits
         }
-        mbar_init(accfull, 1);
+        for (int a = 0; a < kMaxA; ++a) {
+            mbar_init(afull + a, 4);          // one arrival per A-mover warp
+            mbar_init(aempty + a, kIssuers);  // the MMA warps' commits
+        }
+        for (int s = 0; s < kMaxSA; ++s) {
+            mbar_init(sfull + s, 1);   // the A producer's expect_tx (+ TMA bytes)
+            mbar_init(sempty + s, 4);  // one arrival per A-mover warp
+        }
+        mbar_init(accfull, kIssuers);
         for (int i = 0; i < 2; ++i) {
             mbar_init(plan_full + i, 1);
-            mbar_init(plan_empty + i, 2);  // both producers release a plan chunk
+            mbar_init(plan_empty + i, kIssuers);  // the MMA warps release a plan chunk
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
-                     "r"(p.tmem_cols)
+                     "r"(512u)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -365,53 +438,67 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *s_tmem;
 
     if (warp == 3) {
-        // ------------------------------------------------ row planner
-        // For each chunk of block rows: rowptr + colidx into shared memory, then
-        // one lane per row derives the row's kept-block count, B-ring need (G
-        // rounded), first value index and its MMA runs (consecutive block columns,
-        // <= MAX_RUN blocks, each a TMEM column + slot offset + instruction
-        // descriptor), written to a double-buffered plan one chunk ahead of the
-        // producer.  The single-thread producer and MMA roles then do almost no
-        // per-row arithmetic.
+        // ------------------------------------------------ step planner
+        // For each chunk of steps: rowptr + colidx into shared memory, then one
+        // lane per step derives, for each of its block rows, the kept blocks in
+        // this CTA's column range, their B-ring slots (G rounded) and first value
+        // index, and the step's MMA runs (consecutive block columns of one block
+        // row, <= MAX_RUN blocks, split at the issuers' column boundary).  B-ring
+        // slots are handed out in sequence order (a block row that would wrap
+        // starts at slot 0 and the tail slots are skipped), so every slot is fixed
+        // here, not at run time: the run words are final and the B producer only
+        // reclaims slots and issues TMAs.  Double-buffered, one chunk ahead.
+        int bhead = 0;  // B-ring head, the same in every lane
         for (int c = 0; c < nchunks; ++c) {
             const int buf = c & 1;
-            const int64_t Ic = chunk_start(c);
-            const int nrow = chunk_len(c);
-            for (int i = lane; i <= nrow; i += 32) s_rp[i] = __ldg(p.rowptr + Ic + i);
+            const int64_t Rc = chunk_start(c) * R;  // first block row of the chunk
+            const int ns = chunk_len(c);
+            const int nrow = (int)(min((chunk_start(c) + ns) * R, p.nbr) - Rc);
+            for (int i = lane; i <= nrow; i += 32) s_rp[i] = __ldg(p.rowptr + Rc + i);
             __syncwarp();
             const int base = s_rp[0], total = s_rp[nrow] - base;
             for (int e = lane; e < total; e += 32) s_col[e] = (uint16_t)__ldg(p.colidx + base + e);
             if (lane == 0) mbar_wait(plan_empty + buf, ((c >> 1) & 1) ^ 1);
             __syncwarp();
-            int4 *rows = s_rows + buf * kRowCap;
-            uint2 *runs = s_runs + buf * kColCap;
+            int4 *steps = s_steps + buf * kStepCap;
+            uint2 *subs = s_sub + buf * kStepCap * R;
+            uint32_t *runs = s_runs + buf * kColCap;
             int run_base = 0;
-            for (int r0 = 0; r0 < nrow; r0 += 32) {
-                const int r = r0 + lane;
-                int q0 = 0, cnt = 0, nruns = 0;
-                if (r < nrow) {
-                    q0 = s_rp[r] - base;
-                    int q1 = s_rp[r + 1] - base;
-                    if (p.nkr > 1) {
-                        while (q0 < q1 && (int)s_col[q0] < J0) ++q0;
-                        int q = q0;
-                        while (q < q1 && (int)s_col[q] < J0 + nbJ) ++q;
-                        q1 = q;
-                    }
-                    cnt = q1 - q0;
-                    int jprev = -2, rlen = 0;
-                    for (int q = 0; q < cnt; ++q) {
-                        const int J = (int)s_col[q0 + q] - J0;
-                        if (J == jprev + 1 && rlen < C::MAX_RUN && true) {
-                            ++rlen;
-                        } else {
-                            ++nruns;
-                            rlen = 1;
+            for (int s0 = 0; s0 < ns; s0 += 32) {
+                const int st = s0 + lane;
+                int q0[R], cnt[R];
+                int nruns = 0, nonempty = 0;
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int r = st * R + q;
+                    q0[q] = 0;
+                    cnt[q] = 0;
+                    if (st < ns && r < nrow) {
+                        int a = s_rp[r] - base, z = s_rp[r + 1] - base;
+                        nonempty |= z > a;
+                        if (p.nkr > 1) {
+                            while (a < z && (int)s_col[a] < J0) ++a;
+                            int y = a;
+                            while (y < z && (int)s_col[y] < J0 + nbJ) ++y;
+                            z = y;
                         }
-                        jprev = J;
+                        q0[q] = a;
+                        cnt[q] = z - a;
+                        int jprev = -2, rlen = 0;
+                        for (int k = 0; k < cnt[q]; ++k) {
+                            const int J = (int)s_col[a + k] - J0;
+                            if (J == jprev + 1 && rlen < C::MAX_RUN && J != jhalf) {
+                                ++rlen;
+                            } else {
+                                ++nruns;
+                                rlen = 1;
+                            }
+                            jprev = J;
+                        }
                     }
                 }
-                // exclusive warp scan of nruns -> this row's run offset
+                const int inseq = st < ns && (nonempty || (c == 0 && st < n_spec));
+                // exclusive warp scan of nruns -> this step's run offset
                 int incl = nruns;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -420,215 +507,349 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 const int off = run_base + incl - nruns;
                 run_base += __shfl_sync(0xffffffffu, incl, 31);
-                if (r < nrow) {
-                    int jprev = -2, rlen = 0, rstart = 0, k = off;
-                    for (int q = 0; q < cnt; ++q) {
-                        const int J = (int)s_col[q0 + q] - J0;
-                        if (J == jprev + 1 && rlen < C::MAX_RUN && true) {
-                            ++rlen;
-                        } else {
-                            if (rlen)
-                                runs[k++] = make_uint2((uint32_t)((jprev - rlen + 1) * B) | ((uint32_t)rstart << 16),
-                                                       instr_desc<KIND>((uint32_t)(rlen * B)));
-                            rstart = q;
-                            rlen = 1;
-                        }
-                        jprev = J;
+                // B-ring slots, in sequence order: one contiguous range per step (its block
+                // rows back to back, each G rounded); a step that would wrap starts at
+                // slot 0 and the tail slots are skipped (counted as used)
+                int need = 0;
+#pragma unroll
+                for (int q = 0; q < R; ++q) need += (cnt[q] + C::G - 1) / C::G * C::G;
+                int step0 = 0, used = 0;
+                for (uint32_t m = __ballot_sync(0xffffffffu, inseq != 0); m; m &= m - 1) {
+                    const int l = __ffs(m) - 1;
+                    const int nd = __shfl_sync(0xffffffffu, need, l);
+                    const int ws = bhead + nd > p.nbslots ? p.nbslots - bhead : 0;
+                    const int s_0 = ws ? 0 : bhead;
+                    if (lane == l) {
+                        step0 = s_0;
+                        used = nd + ws;
                     }
-                    if (rlen)
-                        runs[k++] = make_uint2((uint32_t)((jprev - rlen + 1) * B) | ((uint32_t)rstart << 16),
-                                               instr_desc<KIND>((uint32_t)(rlen * B)));
-                    rows[r] = make_int4(cnt | (nruns << 16), (cnt + C::G - 1) / C::G * C::G, off, base + q0);
+                    bhead = s_0 + nd;
+                    if (bhead == p.nbslots) bhead = 0;
+                }
+                const int bytes = need * C::BLOCK_BYTES;
+                int slot0[R];
+                slot0[0] = step0;
+#pragma unroll
+                for (int q = 1; q < R; ++q) slot0[q] = slot0[q - 1] + (cnt[q - 1] + C::G - 1) / C::G * C::G;
+                if (st < ns) {
+                    int k = off;
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        const int nd = (cnt[q] + C::G - 1) / C::G * C::G;
+                        subs[st * R + q] = make_uint2((uint32_t)(base + q0[q]), (uint32_t)slot0[q] | ((uint32_t)nd << 16));
+                        int jprev = -2, rlen = 0, rstart = 0;
+                        auto emit = [&]() {
+                            runs[k++] = (uint32_t)((jprev - rlen + 1) * B) | ((uint32_t)(slot0[q] + rstart) << 10) |
+                                        ((uint32_t)rlen << 22) | ((uint32_t)q << 28);
+                        };
+                        for (int i = 0; i < cnt[q]; ++i) {
+                            const int J = (int)s_col[q0[q] + i] - J0;
+                            if (J == jprev + 1 && rlen < C::MAX_RUN && J != jhalf) {
+                                ++rlen;
+                            } else {
+                                if (rlen) emit();
+                                rstart = i;
+                                rlen = 1;
+                            }
+                            jprev = J;
+                        }
+                        if (rlen) emit();
+                    }
+                    steps[st] = make_int4(nruns, used | (inseq << 30), off, bytes);
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(plan_full + buf);
-        }
-    } else if (warp >= 4) {
-        // zero the accumulator columns this CTA owns (MMAs then always accumulate)
-        const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
-        for (int c = 0; c < nbJ * B; c += 16) tmem_st16_zero(tmem + lane_base + c);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
-    if (warp == 1 || warp == 2 || warp >= 4) {  // the MMA warps start only after the accumulator is zeroed
-        tc_fence_before();
-        asm volatile("bar.sync 1, 192;" ::: "memory");
-        tc_fence_after();
-    }
-
-    if ((warp == 0 || warp == 4) && lane == 0) {
-        // ------------------------------------------------ TMA producers (one thread each)
-        // Both walk the same sequence of kept block rows (row j uses stage j % stages).
-        // Warp 0 loads row j's b x 128 dY slab (one 3-D TMA) into the A ring; warp 4
-        // (an epilogue warp, idle until the accumulator is final) places the row's
-        // kept blocks in consecutive B-ring slots (never wrapping: a row that would
-        // wrap starts at slot 0 and the tail slots are skipped), loads them G blocks
-        // per 4-D TMA and writes the stage's ready-to-issue MMA runs.  `full` needs
-        // both arrivals plus all bytes; stages and slots are reclaimed in order as
-        // the MMA commits arrive on `empty`.
-        const bool is_a = warp == 0;
-        int j = 0;  // kept rows issued so far
-        int tail = 0, bhead = 0, bfree = p.nbslots;
-        const uint32_t sA0 = smem_u32(ringA), sB0 = smem_u32(ringB);
-        const uint32_t b_lo0 = (uint32_t)smem_desc(sB0, C::B_LBO, C::B_SBO, C::B_LAYOUT);
-        long long cyc_wait = 0, cyc_issue = 0, cyc_start = clock64();
-        (void)cyc_wait; (void)cyc_issue; (void)cyc_start;
-        // The first n_spec rows are in the sequence whether or not they keep a block:
-        // their dY slabs are requested before the planner has read rowptr/colidx, so
-        // the first HBM round trip overlaps the plan (an empty row costs one slab).
-        const int n_spec = (int)min((int64_t)min(p.stages, first_rows), Ie - Ib);
-        if (is_a)
-            for (int r = 0; r < n_spec; ++r) {
-                mbar_arrive_expect_tx(full + r, (uint32_t)C::A_BYTES);
-                tma_load_3d(&tm_dy, full + r, sA0 + r * C::A_BYTES, 0, (int)(Ib + r) * B, n0 / C::AW);
-            }
-        for (int c = 0; c < nchunks; ++c) {
-            const int buf = c & 1;
-            const int64_t Ic = chunk_start(c);
-            const int nrow = chunk_len(c);
-            mbar_wait(plan_full + buf, (c >> 1) & 1);
-            const int4 *rows = s_rows + buf * kRowCap;
-            const uint2 *runs = s_runs + buf * kColCap;
-            for (int r = 0; r < nrow; ++r) {
-                const int4 rr = rows[r];
-                const int cnt = rr.x & 0xFFFF;
-                const bool spec = c == 0 && r < n_spec;
-                if (cnt == 0 && !spec) continue;
-                const int stage = j % p.stages;
-                if (spec && is_a) {  // slab already requested above
-                    ++j;
-                    continue;
+            // Warm L2 with the chunk's stored blocks (one bulk prefetch per 32 KB, issued by
+            // the first n-tile's CTA): the B loads of the 128-column tiles sharing these
+            // block rows then hit L2 instead of all waiting on the same HBM fill.
+            if (nt == 0 && !(WGRAD_TRACE_MODE & 8)) {
+                const int64_t b0 = (int64_t)base * C::BLOCK_BYTES, nb = (int64_t)total * C::BLOCK_BYTES;
+                for (int64_t o = (int64_t)lane * 32768; o < nb; o += 32 * 32768) {
+                    const uint32_t sz = (uint32_t)min((int64_t)32768, nb - o);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.values + b0 + o), "r"(sz) : "memory");
                 }
-#ifdef WGRAD_TRACE
-                const long long tw0 = clock64();
-#endif
-                if (is_a) {
-                    if (j >= p.stages) mbar_wait(empty + stage, (uint32_t)((j / p.stages) - 1) & 1u);
-                } else {
-                    const int need = rr.y;
-                    const int waste = bhead + need > p.nbslots ? p.nbslots - bhead : 0;
-                    while (j - tail >= p.stages || bfree < need + waste) {  // reclaim the oldest row
-                        mbar_wait(empty + tail % p.stages, (uint32_t)(tail / p.stages) & 1u);
-                        bfree += (int)s_used[tail % p.stages];
+            }
+        }
+    } else if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ B producer (one thread)
+            // Walks the step sequence (step j uses stage j % kStages): once the step's
+            // planned slots are free (stages and slots are reclaimed in order as the
+            // MMA commits arrive on `empty`), loads each block row's kept blocks G per
+            // 4-D TMA.
+            int j = 0;  // steps issued so far
+            int tail = 0, bfree = p.nbslots;
+            long long tr_wait = 0, tr_plan = 0, tr_tma = 0;
+            (void)tr_wait; (void)tr_plan; (void)tr_tma;
+            TCLK(tr_start);
+            const uint32_t sB0 = smem_u32(ringB);
+            for (int c = 0; c < nchunks; ++c) {
+                const int buf = c & 1;
+                const int ns = chunk_len(c);
+                TCLK(tp0);
+                mbar_wait(plan_full + buf, (c >> 1) & 1);
+                TADD(tr_plan, tp0);
+                const int4 *steps = s_steps + buf * kStepCap;
+                const uint2 *subs = s_sub + buf * kStepCap * R;
+                for (int st = 0; st < ns; ++st) {
+                    const int4 rs = steps[st];
+                    if (!(rs.y >> 30)) continue;
+                    const int stage = j % kStages;
+                    const int used = rs.y & 0xFFFFF;
+                    // reclaim the oldest steps until the planned slots are free: enough
+                    // free slots past the head, or an empty ring (a step that wrapped may
+                    // count more than nbslots; bfree then goes negative until it is reclaimed)
+                    while (j - tail >= kStages || (bfree < used && bfree < p.nbslots)) {
+                        TCLK(tw0);
+                        mbar_wait(empty + tail % kStages, (uint32_t)(tail / kStages) & 1u);
+                        TADD(tr_wait, tw0);
+                        bfree += (int)s_used[tail % kStages];
                         ++tail;
                     }
-                    const int slot0 = waste ? 0 : bhead;
-                    s_used[stage] = (uint32_t)(need + waste);
-                    bhead = slot0 + need;
-                    if (bhead == p.nbslots) bhead = 0;
-                    bfree -= need + waste;
-                    // ready-to-issue runs: TMEM address, B descriptor low word, instruction descriptor
-                    const int nruns = rr.x >> 16;
-                    uint4 *m = meta + stage * kMetaQuads;
-                    for (int i = 0; i < nruns; ++i) {  // compact run word: column | B-ring slot << 10 | length << 22
-                        const uint2 run = runs[rr.z + i];
-                        const uint32_t len = ((run.y >> 17) & 0x3Fu) * 8u / (uint32_t)B;
-                        m[1 + i].x = (run.x & 0x3FFu) | ((uint32_t)(slot0 + (int)(run.x >> 16)) << 10) | (len << 22);
-                    }
-                    m[0].x = (uint32_t)nruns;
-#ifdef WGRAD_TRACE
-                    const long long tw1 = clock64();
-                    cyc_wait += tw1 - tw0;
-#endif
-                    mbar_arrive_expect_tx(full + stage, (uint32_t)(need * C::BLOCK_BYTES));
-                    for (int g = 0; g < need; g += C::G)
-                        tma_load_4d(&tm_val, full + stage, sB0 + (slot0 + g) * C::BLOCK_BYTES, 0, 0, 0, rr.w + g);
-#ifdef WGRAD_TRACE
-                    cyc_issue += clock64() - tw1;
-#endif
-                }
-                if (is_a) {
-#ifdef WGRAD_TRACE
-                    const long long tw1 = clock64();
-                    cyc_wait += tw1 - tw0;
-#endif
-                    mbar_arrive_expect_tx(full + stage, (uint32_t)C::A_BYTES);
-                    tma_load_3d(&tm_dy, full + stage, sA0 + stage * C::A_BYTES, 0, (int)(Ic + r) * B, n0 / C::AW);
-#ifdef WGRAD_TRACE
-                    cyc_issue += clock64() - tw1;
-#endif
-                }
-                ++j;
-            }
-            mbar_arrive(plan_empty + buf);
-        }
-#ifdef WGRAD_TRACE
-        g_trace[blockIdx.x][210 + 4 * (warp == 4)] = (unsigned long long)cyc_wait;
-        g_trace[blockIdx.x][211 + 4 * (warp == 4)] = (unsigned long long)cyc_issue;
-        g_trace[blockIdx.x][212 + 4 * (warp == 4)] = (unsigned long long)(clock64() - cyc_start);
-        g_trace[blockIdx.x][213 + 4 * (warp == 4)] = (unsigned long long)j;
-#endif
-        // end marker in stage j % stages: free it, then both producers arrive (no bytes)
-        const int stage = j % p.stages;
-        if (j >= p.stages) mbar_wait(empty + stage, (uint32_t)((j / p.stages) - 1) & 1u);
-        if (!is_a) meta[stage * kMetaQuads] = make_uint4(kEndMarker, 0u, 0u, 0u);
-        mbar_arrive(full + stage);
-    } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer (whole warp, one elected lane issues)
-        // Lane i loads word i of the stage's metadata (header + runs) with ONE shared
-        // load; each run word becomes warp-uniform with a single masked redux, and
-        // the descriptors are built from it with uniform arithmetic, so every
-        // tcgen05.mma is one predicated UTCHMMA.
-        const uint64_t a_desc0 = smem_desc(smem_u32(ringA), C::A_LBO, C::A_SBO, C::A_LAYOUT);
-        const uint32_t a_lo0 = (uint32_t)a_desc0, a_hi = (uint32_t)(a_desc0 >> 32);
-        const uint64_t b_desc0 = smem_desc(smem_u32(ringB), C::B_LBO, C::B_SBO, C::B_LAYOUT);
-        const uint32_t b_lo0 = (uint32_t)b_desc0, b_hi = (uint32_t)(b_desc0 >> 32);
-        const uint32_t idesc0 = instr_desc<KIND>(0u);
-        int stage = 0;
-        uint32_t phase = 0;
-        long long mw = 0, mi = 0, m_start = clock64(), nrow_m = 0;
-        (void)mw; (void)mi; (void)m_start; (void)nrow_m;
-        for (;;) {
-#ifdef WGRAD_TRACE
-            const long long t0m = clock64();
-#endif
-            mbar_wait(full + stage, phase);
-            tc_fence_after();
-#ifdef WGRAD_TRACE
-            const long long t1m = clock64();
-            mw += t1m - t0m;
-            ++nrow_m;
-#endif
-            const uint32_t m_addr = smem_u32(meta + stage * kMetaQuads);
-            uint32_t wl;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wl) : "r"(m_addr + lane * 16u));
-            const uint32_t nruns = __reduce_or_sync(0xffffffffu, lane == 0 ? wl : 0u);
-            if (nruns == kEndMarker) break;
-            const uint32_t a_lo = a_lo0 + (uint32_t)((stage * C::A_BYTES) >> 4);
-            for (uint32_t i = 0; i < nruns; ++i) {
-                uint32_t w = wl;
-                if (i + 1 >= 32) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(m_addr + (i + 1) * 16u));
-                const uint32_t rw = __reduce_or_sync(0xffffffffu, (i + 1 >= 32 || lane == i + 1) ? w : 0u);
-                const uint32_t d = tmem + (rw & 0x3FFu);
-                const uint32_t b_lo = b_lo0 + ((rw >> 10) & 0xFFFu) * (uint32_t)(C::BLOCK_BYTES >> 4);
-                const uint32_t idesc = idesc0 | ((((rw >> 22) & 0x3Fu) * (uint32_t)B >> 3) << 17);
+                    s_used[stage] = (uint32_t)used;
+                    bfree -= used;
+                    TCLK(tt0);
+                    TLAT(0, j);
+                    if (WGRAD_TRACE_MODE & 2) {
+                        mbar_arrive(full + stage);
+                    } else {
+                        mbar_arrive_expect_tx(full + stage, (uint32_t)rs.w);
 #pragma unroll
-                for (int s = 0; s < B / C::UK; ++s)
-                    tc_mma_elect<KIND>(d, a_lo + ((s * C::A_KSTEP) >> 4), a_hi, b_lo + ((s * C::B_KSTEP) >> 4), b_hi,
-                                       idesc);
+                        for (int q = 0; q < R; ++q) {
+                            const uint2 sb = subs[st * R + q];
+                            const int nd = (int)(sb.y >> 16);
+                            const uint32_t dst = sB0 + (sb.y & 0xFFFFu) * C::BLOCK_BYTES;
+                            for (int g = 0; g < nd; g += C::G)
+                                tma_load_4d(&tm_val, full + stage, dst + g * C::BLOCK_BYTES, 0, 0, 0, (int)sb.x + g);
+                        }
+                    }
+                    TADD(tr_tma, tt0);
+                    ++j;
+                }
+            }
+            TSET(214, tr_wait);
+            TSET(215, clock64() - tr_start);
+            TSET(216, tr_plan);
+            TSET(217, j);
+            TSET(208, 0);
+            TSET(209, tr_tma);
+        }
+    } else if (warp == 1 || warp == 2) {
+        // ------------------------------------------------ MMA issuers (whole warps, one elected lane issues)
+        // Warp 1 issues the runs in accumulator blocks [0, jhalf), warp 2 those in
+        // [jhalf, nbJ): a run's issue cost is a dependent chain (redux -> descriptor
+        // -> uniform registers -> UTCHMMA) of a few hundred cycles, and two warps on
+        // different SM sub-partitions overlap their chains.  Both walk the plan: a
+        // ballot over 32 step records finds the steps in the sequence, lane i loads
+        // run word i of the step with ONE shared load, a ballot selects this warp's
+        // runs and each run word becomes warp-uniform with a single masked redux.
+        tc_fence_before();
+        asm volatile("bar.sync 1, 320;" ::: "memory");  // accumulator zeroed by warps 4-7
+        tc_fence_after();
+        const bool upper = warp == 2;
+        const uint32_t col_split = (uint32_t)(jhalf * B);
+        // warp-uniform copies (REDUX results live in uniform registers)
+        const uint32_t tmem_u = __reduce_or_sync(0xffffffffu, tmem);
+        const uint64_t b_desc0 = smem_desc(smem_u32(ringB), C::B_LBO, C::B_SBO, C::B_LAYOUT);
+        const uint32_t b_lo0 = __reduce_or_sync(0xffffffffu, (uint32_t)b_desc0);
+        const uint32_t b_hi = __reduce_or_sync(0xffffffffu, (uint32_t)(b_desc0 >> 32));
+        const uint32_t idesc0 = instr_desc<KIND>(0u);
+        const uint32_t a_tm0 = tmem_u + p.a_col0;
+        int stage = 0, a = 0;
+        uint32_t phase = 0, aphase = 0;
+        long long tr_wf = 0, tr_wa = 0, tr_is = 0, tr_loop = 0, tr_nm = 0;
+        (void)tr_wf; (void)tr_wa; (void)tr_is; (void)tr_loop; (void)tr_nm;
+#ifdef WGRAD_TRACE
+        int jm = 0;
+#endif
+        TCLK(tr_start);
+        if (lane == 0 && !upper) TRACE(205);
+        for (int c = 0; c < nchunks; ++c) {
+            const int buf = c & 1;
+            const int ns = chunk_len(c);
+            mbar_wait(plan_full + buf, (c >> 1) & 1);
+            const int4 *steps = s_steps + buf * kStepCap;
+            const uint32_t *runs = s_runs + buf * kColCap;
+            for (int s0 = 0; s0 < ns; s0 += 32) {
+                const int4 rec = s0 + lane < ns ? steps[s0 + lane] : make_int4(0, 0, 0, 0);
+                for (uint32_t seq = __ballot_sync(0xffffffffu, (rec.y >> 30) != 0); seq; seq &= seq - 1) {
+                    const int l = __ffs(seq) - 1;
+                    const uint32_t nruns = __reduce_or_sync(0xffffffffu, lane == l ? (uint32_t)rec.x : 0u);
+                    const uint32_t off = __reduce_or_sync(0xffffffffu, lane == l ? (uint32_t)rec.z : 0u);
+                    TCLK(tw0);
+                    mbar_wait(full + stage, phase);
+                    TADD(tr_wf, tw0);
+#ifdef WGRAD_TRACE
+                    if (!upper && lane == 0) TLAT(1, jm);
+                    ++jm;
+#endif
+                    TCLK(tw1);
+                    mbar_wait(afull + a, aphase);
+                    TADD(tr_wa, tw1);
+                    TCLK(tw2);
+                    tc_fence_after();
+                    const uint32_t a_tm = a_tm0 + (uint32_t)(a * C::A_STEP);
+                    TCLK(tw3);
+                    for (uint32_t w0 = 0; w0 < nruns; w0 += 32) {
+                        const uint32_t wl = w0 + lane < nruns ? runs[off + w0 + lane] : 0u;
+                        uint32_t mine = __ballot_sync(0xffffffffu, w0 + lane < nruns &&
+                                                                       (((wl & 0x3FFu) >= col_split) == upper));
+                        if (WGRAD_TRACE_MODE & 1) mine = 0;
+#ifdef WGRAD_TRACE
+                        tr_nm += __popc(mine);
+#endif
+                        while (mine) {
+                            const int i = __ffs(mine) - 1;
+                            mine &= mine - 1;
+                            const uint32_t rw = __reduce_or_sync(0xffffffffu, lane == i ? wl : 0u);
+                            const uint32_t d = tmem_u + (rw & 0x3FFu);
+                            const uint32_t b_lo = b_lo0 + ((rw >> 10) & 0xFFFu) * (uint32_t)(C::BLOCK_BYTES >> 4);
+                            const uint32_t idesc = idesc0 | ((((rw >> 22) & 0x3Fu) * (uint32_t)B >> 3) << 17);
+                            const uint32_t a_q = a_tm + ((rw >> 28) & 0x3u) * (uint32_t)C::A_COLS;
+                            tc_mma_ts_run<KIND, B / C::UK, C::A_KCOLS, (C::B_KSTEP >> 4)>(d, a_q, b_lo, b_hi, idesc);
+                        }
+                    }
+                    TADD(tr_loop, tw3);
+                    __syncwarp();
+                    if (lane == 0) {
+                        tc_commit(empty + stage);  // frees the stage (and its B slots) once these MMAs complete
+                        tc_commit(aempty + a);     // frees the A buffer
+                    }
+                    __syncwarp();
+                    TADD(tr_is, tw2);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                    if (++a == p.na) { a = 0; aphase ^= 1; }
+                }
             }
             __syncwarp();
-            if (lane == 0) tc_commit(empty + stage);  // frees the stage (and its B slots) once these MMAs complete
-            __syncwarp();
-#ifdef WGRAD_TRACE
-            mi += clock64() - t1m;
-#endif
-            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+            if (lane == 0) mbar_arrive(plan_empty + buf);  // this chunk's plan is no longer read
         }
-#ifdef WGRAD_TRACE
-        if (lane == 0) {
-            g_trace[blockIdx.x][218] = (unsigned long long)mw;
-            g_trace[blockIdx.x][219] = (unsigned long long)mi;
-            g_trace[blockIdx.x][220] = (unsigned long long)(clock64() - m_start);
+        if (lane == 0 && !upper) {
+            TSET(218, tr_wf);
+            TSET(219, tr_wa);
+            TSET(220, clock64() - tr_start);
+            TSET(221, tr_is);
+            TSET(223, tr_loop);
+            TSET(224, tr_nm);
         }
-#endif
         if (lane == 0) tc_commit(accfull);
+    } else if (warp >= 4) {
+        // ------------------------------------------------ A producer (warp 8) and A movers (warps 4-7, 9-12)
+        // Step j of the sequence: warp 8 lane 0 requests its dY slab (one 2-D TMA,
+        // SROWS x 128, row-major) into A-ring stage j % sa as soon as the stage is
+        // free; the movers move it shared -> registers (warp w owns TMEM lanes
+        // 32 (w % 4) .. + 31, thread lane m = dY column n0 + m) -> tcgen05.st into
+        // A buffer j % na.  Warps 4-7 take the even steps, warps 9-12 the odd ones.
+        // Step-sequence cursor, the B producer's sequence: the n_spec speculative
+        // steps, then every step with at least one stored block (rowptr read 32
+        // steps at a time, one ballot).  Producer and movers each run it; it never
+        // waits on the planner.
+        int64_t wS = Sb + n_spec, wbase = 0, sS = Sb;
+        uint32_t wmask = 0;
+        auto next_step = [&](int64_t &S) -> bool {
+            if (sS < Sb + n_spec) {
+                S = sS++;
+                return true;
+            }
+            while (!wmask) {
+                if (wS >= Se) return false;
+                const int64_t s = wS + lane;
+                const bool ne = s < Se && __ldg(p.rowptr + min((s + 1) * R, p.nbr)) > __ldg(p.rowptr + s * R);
+                wmask = __ballot_sync(0xffffffffu, ne);
+                wbase = wS;
+                wS += 32;
+            }
+            S = wbase + (__ffs(wmask) - 1);
+            wmask &= wmask - 1;
+            return true;
+        };
+        const uint32_t sA0 = smem_u32(ringA);
+        if (warp == 8) {
+            long long tr_w = 0;
+            (void)tr_w;
+            int64_t S;
+            for (int j = 0; next_step(S); ++j) {
+                if (lane == 0) {
+                    const int s = j % p.sa;
+                    TCLK(tw0);
+                    if (j >= p.sa) mbar_wait(sempty + s, (uint32_t)((j / p.sa) - 1) & 1u);
+                    TADD(tr_w, tw0);
+                    TLAT(2, j);
+                    if (WGRAD_TRACE_MODE & 4) {
+                        mbar_arrive(sfull + s);
+                    } else {
+                        mbar_arrive_expect_tx(sfull + s, (uint32_t)C::SLAB);
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                                sA0 + (uint32_t)(s * C::SLAB)),
+                            "l"(reinterpret_cast<uint64_t>(&tm_dy)), "r"(n0), "r"((int)(S * C::SROWS)),
+                            "r"(smem_u32(sfull + s))
+                            : "memory");
+                    }
+                }
+                __syncwarp();
+            }
+            if (lane == 0) TSET(206, tr_w);
+        } else {
+            const int ew = warp & 3;
+            const int par = warp >= 9;
+            const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
+            // zero the accumulator columns this CTA owns (MMAs then always accumulate)
+            if (!par) {
+                for (int c = 0; c < nbJ * B; c += 16) tmem_st16_zero(tmem + lane_base + c);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+            tc_fence_before();
+            asm volatile("bar.sync 1, 320;" ::: "memory");
+            tc_fence_after();
+            const uint32_t a_tm0 = tmem + lane_base + p.a_col0;
+            const uint32_t my_col = (uint32_t)((ew * 32 + lane) * C::ES);
+            long long tr_wa = 0, tr_st = 0, tr_ld = 0, tr_sw = 0;
+            (void)tr_wa; (void)tr_st; (void)tr_ld; (void)tr_sw;
+            TCLK(tr_start);
+            int j = 0;
+            int64_t S;
+            for (; next_step(S); ++j) {
+                if ((j & 1) != par) continue;
+                TCLK(tl0);
+                const int s = j % p.sa;
+                TCLK(tsw);
+                mbar_wait(sfull + s, (uint32_t)(j / p.sa) & 1u);
+                TADD(tr_sw, tsw);
+                if (lane == 0 && ew == 0) TLAT(3, j);
+                uint32_t v[C::SROWS];
+                lds_slab<KIND, C::SROWS>(v, sA0 + (uint32_t)(s * C::SLAB) + my_col);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sempty + s);
+                TADD(tr_ld, tl0);
+                const int ab = j % p.na;
+                TCLK(tw0);
+                if (j >= p.na) mbar_wait(aempty + ab, (uint32_t)((j / p.na) - 1) & 1u);
+                TADD(tr_wa, tw0);
+                TCLK(ts0);
+                tc_fence_after();
+                store_slab<KIND, C::SROWS>(a_tm0 + (uint32_t)(ab * C::A_STEP), v);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                TADD(tr_st, ts0);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(afull + ab);
+            }
+            if (threadIdx.x == 128) {
+                TSET(210, tr_wa);
+                TSET(211, clock64() - tr_start);
+                TSET(212, j);
+                TSET(213, tr_st);
+                TSET(222, tr_ld);
+                TSET(207, tr_sw);
+            }
+        }
     }
-    if (warp >= 4) {
-        __syncwarp();  // warp 4's lane 0 rejoins after its B-producer loop
+    if (warp >= 4 && warp < 8) {
         // ------------------------------------------------ epilogue
         // TMEM -> registers -> a [32 kcol][128 n] fp32 staging tile in the (now
-        // idle) A ring -> one TMA bulk tensor store (or reduce-add) per 16 kcols.
+        // idle) rings -> one TMA bulk tensor store (or reduce-add) per 16 kcols.
         // Full 512-byte row segments leave the SM through the TMA unit instead of
         // 128-byte scattered STGs.  mode 3 stores this split's partial tile into
         // its own workspace slice (summed afterwards in split order:
@@ -638,7 +859,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (threadIdx.x == 128) TRACE(203);
         const int ew = warp - 4;
         const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
-        float *stage_buf = reinterpret_cast<float *>(ringA);  // 2 x [32][128]
+        float *stage_buf = reinterpret_cast<float *>(ringA);  // 2 x [32][128] over the idle A/B rings
         const int ncols = nbJ * B;
         const int row0 = (p.mode == 3 ? split * (int)p.K : 0) + J0 * B;
         const CUtensorMap *tm_o = p.mode == 3 ? &tm_ws : &tm_dw;
@@ -682,7 +903,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
     }
 }
 
@@ -740,49 +961,43 @@ static cudaError_t make_map(CUtensorMap *tm, const void *base, CUtensorMapDataTy
 }
 
 struct Plan {
-    int kr_blocks, nkr, stages, nbslots, nsplit, smem, chunk_rows;
-    uint32_t tmem_cols;
+    int kr_blocks, nkr, nbslots, na, sa, nsplit, smem, chunk_steps;
+    uint32_t a_col0;
 };
 
 // sms: SMs the split-K grid may fill (the device's count at launch, kSplitSMs
-// for the pure workspace query).  avg_cnt: expected kept blocks per block row
-// inside one TMEM column range (sizes the A ring against the B ring).
+// for the pure workspace query).
 template <int KIND, int B>
-static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms, double avg_cnt = -1.0) {
+static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms) {
     using C = Cfg<KIND, B>;
     Plan pl{};
     const int nbc = (int)(K / B);
-    const int ring = kSmemBudget - kFixedSmem;
-    // largest kcol range (<= 512 TMEM columns) whose full row (A slab + every
-    // block) fits twice in the rings
-    int maxb = std::min(512 / B, nbc);
+    // A ring: 64 KB of dY slabs per SM, 2..kMaxSA stages; the rest of shared memory
+    // goes to the B ring (measured: with fp32 blocks the B ring's depth, not the A
+    // ring's, bounds the main loop)
+    pl.sa = std::max(2, std::min(kMaxSA, 65536 / C::SLAB));
+#ifdef WGRAD_SA
+    pl.sa = WGRAD_SA;  // dev sweeps only
+#endif
+    const int ring = kSmemBudget - kFixedSmem - pl.sa * C::SLAB;
+    // largest kcol range whose accumulator leaves room for two A buffers in the
+    // 512 TMEM columns and whose densest step (R block rows, every block, G rounded)
+    // fits the B ring; <= 56 blocks keeps a run word's column in 10 bits
+    int maxb = std::min(std::min((512 - 2 * C::A_STEP) / B, 56), nbc);
     auto need_of = [](int blocks) { return (blocks + C::G - 1) / C::G * C::G; };
-    while (maxb > 1 && 2 * (C::A_BYTES + kStageExtra) + 2 * need_of(maxb) * C::BLOCK_BYTES > ring) --maxb;
+    while (maxb > 1 && C::R * need_of(maxb) * C::BLOCK_BYTES > ring) --maxb;
     pl.nkr = (nbc + maxb - 1) / maxb;
     pl.kr_blocks = (nbc + pl.nkr - 1) / pl.nkr;
-    if (avg_cnt < 0) avg_cnt = pl.kr_blocks;
-    avg_cnt = std::max(1.0, std::min<double>(avg_cnt, pl.kr_blocks));
-    // rows in flight: stages x (A slab + avg_cnt blocks) fills the ring
-    // rows in flight: stages x (A slab + the average row's block slots) fills the ring
-    const double avg_need = std::ceil(avg_cnt / C::G) * C::G + 0.5 * (C::G - 1);
-    int stages = (int)(ring / (C::A_BYTES + kStageExtra + avg_need * C::BLOCK_BYTES));
-    stages = std::max(2, std::min(64, stages));
-    int nb = (ring - stages * (C::A_BYTES + kStageExtra)) / C::BLOCK_BYTES;
-    while (nb < 2 * need_of(pl.kr_blocks) && stages > 2) {  // a full row must fit even after a wrap
-        --stages;
-        nb = (ring - stages * (C::A_BYTES + kStageExtra)) / C::BLOCK_BYTES;
-    }
-    pl.stages = stages;
-    pl.nbslots = nb;
-    pl.smem = stages * (C::A_BYTES + kStageExtra) + pl.nbslots * C::BLOCK_BYTES + kFixedSmem;
-    pl.chunk_rows = std::max(1, std::min(kRowCap, kColCap / nbc));  // a chunk's kept blocks fit the colidx/run buffers
-    uint32_t cols = 32;
-    while (cols < (uint32_t)(pl.kr_blocks * B)) cols <<= 1;
-    pl.tmem_cols = cols;
+    pl.na = std::min(kMaxA, (512 - pl.kr_blocks * B) / C::A_STEP);
+    pl.a_col0 = (uint32_t)(512 - pl.na * C::A_STEP);
+    pl.nbslots = std::min(4095, ring / C::BLOCK_BYTES);
+    pl.smem = pl.sa * C::SLAB + pl.nbslots * C::BLOCK_BYTES + kFixedSmem;
+    // a chunk's stored blocks (all columns) fit the colidx / run-word buffers
+    pl.chunk_steps = std::min(kStepCap, kColCap / (C::R * nbc));
     const int64_t tiles = (N / 128) * pl.nkr;
-    const int64_t nbr = M / B;
+    const int64_t nst = (M / B + C::R - 1) / C::R;
     const int64_t cap = std::min<int64_t>(sms, kSplitSMs);
-    pl.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nbr, cap / std::max<int64_t>(1, tiles)));
+    pl.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nst, cap / std::max<int64_t>(1, tiles)));
     return pl;
 }
 
@@ -794,18 +1009,16 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     int dev = 0, sms = kSplitSMs;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // kept blocks per block row inside one TMEM column range, on average
-    Plan pl = plan_for<KIND, B>(M, K, N, sms);
-    const double avg_cnt = (double)nnzb / (double)(M / B) * pl.kr_blocks / (double)(K / B);
-    pl = plan_for<KIND, B>(M, K, N, sms, avg_cnt);
+    const Plan pl = plan_for<KIND, B>(M, K, N, sms);
+    if (pl.chunk_steps < 1) return cudaErrorNotSupported;  // K / b too large for the chunk buffers
     const CUtensorMapDataType dt = KIND == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    // dY (N x M, row-major): one box = the SROWS x 128 slab of a step, row-major
+    // in shared memory (no swizzle: the A movers read it column-wise)
     CUtensorMap tm_dy, tm_val;
-    // dY as (column within a 128-byte atom, row, atom): one box = the b x 128 slab
-    // of a block row, atom-major in shared memory (A_LBO apart)
-    const cuuint64_t dy_dims[3] = {(cuuint64_t)C::AW, (cuuint64_t)M, (cuuint64_t)(N / C::AW)};
-    const cuuint64_t dy_str[2] = {(cuuint64_t)N * C::ES, 128};
-    const cuuint32_t dy_box[3] = {(cuuint32_t)C::AW, (cuuint32_t)B, (cuuint32_t)C::A_ATOMS};
-    cudaError_t e = make_map(&tm_dy, dY, dt, 3, dy_dims, dy_str, dy_box, C::TF32 ? -128 : 128);
+    const cuuint64_t dy_dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+    const cuuint64_t dy_str[1] = {(cuuint64_t)N * C::ES};
+    const cuuint32_t dy_box[2] = {128, (cuuint32_t)C::SROWS};
+    cudaError_t e = make_map(&tm_dy, dY, dt, 2, dy_dims, dy_str, dy_box, 0);
     if (e != cudaSuccess) return e;
     // values as (element within a swizzle atom row, block row, atom, block): one
     // box = G consecutive stored blocks, each atom-major (B_LBO apart)
@@ -830,6 +1043,7 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     Params p{};
     p.rowptr = rowptr;
     p.colidx = colidx;
+    p.values = static_cast<const uint8_t *>(values);
     p.dW = dW;
     p.nbr = M / B;
     p.N = N;
@@ -837,18 +1051,13 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     p.nkr = pl.nkr;
     p.nsplit = pl.nsplit;
     p.kr_blocks = pl.kr_blocks;
-    p.stages = pl.stages;
     p.nbslots = pl.nbslots;
-    p.tmem_cols = pl.tmem_cols;
-    p.chunk_rows = pl.chunk_rows;
+    p.na = pl.na;
+    p.sa = pl.sa;
+    p.a_col0 = pl.a_col0;
+    p.chunk_steps = pl.chunk_steps;
     p.ws = ws;
     p.mode = pl.nsplit > 1 ? 3 : accumulate ? 1 : 0;
-#ifdef WGRAD_TMA_REDUCE
-    if (pl.nsplit > 1) {  // experiment: TMA bulk reduce-add of every split into dW
-        p.mode = 1;
-        if (!accumulate) cudaMemsetAsync(dW, 0, (size_t)K * N * 4, stream);
-    }
-#endif
     auto kern = wgrad_tc_kernel<KIND, B>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     if (e != cudaSuccess) return e;
@@ -856,7 +1065,7 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     kern<<<grid, kThreads, pl.smem, stream>>>(tm_dy, tm_val, tm_dw, tm_ws, p);
     count_launch();
     e = cudaGetLastError();
-    if (e != cudaSuccess || pl.nsplit == 1 || p.mode == 1) return e;
+    if (e != cudaSuccess || pl.nsplit == 1) return e;
     const int64_t n4 = K * N / 4;
     const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 8));
     splitk_reduce_kernel<<<rgrid, 256, 0, stream>>>(reinterpret_cast<const float4 *>(ws),
