@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libbsrprune.so")
+LIB_PATH = os.environ.get("BSRP_LIB") or os.path.join(_PKG, "libbsrprune.so")  # BSRP_LIB: dev builds only
 
 BSR_OK = 0
 STATUS_NAMES = {0: "BSR_OK", 1: "BSR_ERR_INVALID_ARG", 2: "BSR_ERR_SHAPE", 3: "BSR_ERR_UNSUPPORTED",

@@ -37,4 +37,13 @@ cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const 
                             int64_t nnzb, int kind, int64_t M, int64_t K, int b, const void *dY,
                             int64_t N, float *dW, int accumulate, void *ws, cudaStream_t stream);
 
+// Span kernel (wgrad_span.cu): dense-padded per-row spans, CTA-pair MMAs.
+size_t wgrad_span_ws_bytes(int64_t M, int64_t K, int b, int64_t N);
+cudaError_t launch_wgrad_span(const int32_t *rowptr, const int32_t *colidx, const void *values,
+                              int64_t nnzb, int kind, int64_t M, int64_t K, int b, const void *dY,
+                              int64_t N, float *dW, int accumulate, void *ws, cudaStream_t stream);
+// dW (+)= sum over nsplit partial K x N tiles in split order (deterministic).
+cudaError_t launch_splitk_reduce(const float *ws, float *dW, int64_t n, int nsplit, int accumulate,
+                                 cudaStream_t stream);
+
 }  // namespace bsrp

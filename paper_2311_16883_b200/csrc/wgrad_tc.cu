@@ -40,6 +40,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "common.cuh"
 #include "launch.h"
@@ -1076,7 +1077,19 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
 
 }  // namespace tc
 
-size_t wgrad_tc_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
+cudaError_t launch_splitk_reduce(const float *ws, float *dW, int64_t n, int nsplit, int accumulate, cudaStream_t stream) {
+    int dev = 0, sms = tc::kSplitSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t n4 = n / 4;
+    const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 8));
+    tc::splitk_reduce_kernel<<<rgrid, 256, 0, stream>>>(reinterpret_cast<const float4 *>(ws),
+                                                        reinterpret_cast<float4 *>(dW), n4, nsplit, accumulate);
+    count_launch();
+    return cudaGetLastError();
+}
+
+static size_t wgrad_runs_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
     tc::Plan pl{};
 #define WS_CASE(B_) if (b == B_) pl = tc::plan_for<1, B_>(M, K, N, tc::kSplitSMs);
     WS_CASE(16) WS_CASE(32) WS_CASE(64)
@@ -1090,9 +1103,22 @@ size_t wgrad_tc_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
     return ns > 1 ? (size_t)ns * K * N * sizeof(float) : 0;
 }
 
+size_t wgrad_tc_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
+    return std::max(wgrad_runs_ws_bytes(M, K, b, N), wgrad_span_ws_bytes(M, K, b, N));
+}
+
+// Kernel choice: the per-run kernel above unless BSRP_WGRAD=span selects the
+// experimental span kernel (wgrad_span.cu; measured slower at C2).
+static bool use_runs_kernel() {
+    const char *e = std::getenv("BSRP_WGRAD");
+    return !(e && std::string(e) == "span");
+}
+
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
                             int kind, int64_t M, int64_t K, int b, const void *dY, int64_t N, float *dW,
                             int accumulate, void *ws, cudaStream_t stream) {
+    if (!use_runs_kernel())
+        return launch_wgrad_span(rowptr, colidx, values, nnzb, kind, M, K, b, dY, N, dW, accumulate, ws, stream);
     if (!values || nnzb == 0) {  // no stored block: dW = 0 (or unchanged)
         return accumulate ? cudaSuccess : cudaMemsetAsync(dW, 0, (size_t)K * N * sizeof(float), stream);
     }

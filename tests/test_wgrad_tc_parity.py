@@ -26,6 +26,14 @@ import paper_2311_16883_b200 as bp  # noqa: E402
 TOL = 5e-3
 
 
+@pytest.fixture(autouse=True, params=["runs", "span"])
+def wgrad_kernel(request, monkeypatch):
+    """Every case runs on both tcgen05 dW kernels: the default per-run kernel and the
+    experimental span kernel (CTA-pair MMAs; BSRP_WGRAD=span)."""
+    monkeypatch.setenv("BSRP_WGRAD", request.param)
+    return request.param
+
+
 def tc_supported(prec, b):
     """TF32 MN-major operands need 128-byte block rows: b >= 32 (include/bsrprune.h)."""
     return not (prec == "tf32" and b < 32)
@@ -81,6 +89,19 @@ def test_wgrad_tc_random(prec, b, keep, shape):
         assert err <= 1e-4, err
     else:  # tf32 operand rounding is visible (P12)
         assert err >= 1e-6, f"tf32 error {err} suspiciously small"
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("b", [16, 32, 64])
+@pytest.mark.parametrize("keep", [0.1, 0.5, 0.9])
+def test_wgrad_tc_many_rows_per_cta(prec, b, keep):
+    """N = 256: one CTA pair per split, so every CTA walks dozens of block rows and
+    the shared-memory stage ring wraps many times (odd spans padded left and right)."""
+    nbr, nbc, N = 100 * 64 // b, 384 // b, 256
+    M, K = nbr * b, nbc * b
+    k = oracle.keep_count(nbr * nbc, keep)
+    got, ref = run_tc(M, K, N, b, k, prec, seed=900 + b)
+    assert oracle.rel_frobenius(got, ref) <= TOL
 
 
 @pytest.mark.parametrize("prec", ["tf32", "bf16"])
