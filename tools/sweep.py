@@ -1,0 +1,202 @@
+#!/usr/bin/env python
+"""Measurement sweeps of SURVEY §8(d) on one B200 (run through gpurun):
+
+  c3  ResMLP-S12 linear layers at batch 128 (BASELINE configs[2]): fc1 (X 25088 x 384,
+      dY 25088 x 1536) and fc2 (X 25088 x 1536, dY 25088 x 384), block size
+      4/8/16/32/64 x keep 0.1..1.0 (sparsity 90%..0%), fp32 and bf16 storage.  Per
+      (layer, b, keep, dtype): prune / wgrad / decompress device time, GB/s,
+      TFLOP/s and roofline fractions; plus the 12-block model totals.
+  c5  prune/pack bandwidth sweep (configs[4]): X of 256 MiB, 1 GiB and 4 GiB
+      (K = 1536 fp32), blocks 4/16/32/64, keep 0.1/0.5/1.0.
+
+    python tools/sweep.py c3 c5 --out-dir profiles/r01_sweep
+
+Timing: CUDA events around back-to-back launches on the current stream over
+rotating input sets (each set larger than the 126 MB L2 for c3; c5 inputs are
+larger than L2 by themselves), after warm-up.  Inputs are seeded synthetic
+activations generated on the device with the shape/distribution recipe of
+DESIGN.md §4 (per-channel affine + per-sample scale; GELU for fc2 inputs).
+`check` is a self-consistency check of every measured dW against float64 torch
+on the decompressed BSR (parity against the oracle is the job of tests/).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2311_16883_b200 as bp  # noqa: E402
+from paper_2311_16883_b200 import metrics  # noqa: E402
+
+SEED = 231116883
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1800.0, "fallback (B200_PROFILING.md)"
+
+
+def activation(M, K, family, seed, dtype):
+    """F_aff / F_gelu of DESIGN.md §4 on the device: sigma_s * f(alpha_c z + beta_c),
+    sigma_s per 196-row sample, alpha_c / beta_c per channel."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    z = torch.randn(M, K, device="cuda", generator=g)
+    alpha = torch.exp(0.5 * torch.randn(K, device="cuda", generator=g))
+    beta = (0.1 if family == "aff" else 0.5) * torch.randn(K, device="cuda", generator=g)
+    sig = torch.exp(0.25 * torch.randn((M + 195) // 196, device="cuda", generator=g)).repeat_interleave(196)[:M]
+    x = z.mul_(alpha).add_(beta)
+    if family == "gelu":
+        x = torch.nn.functional.gelu(x, approximate="tanh")
+    x.mul_(sig[:, None])
+    return x.to(dtype)
+
+
+def grad_out(M, N, seed, dtype):
+    g = torch.Generator(device="cuda").manual_seed(seed + 1)
+    return (0.01 * torch.randn(M, N, device="cuda", generator=g)).to(dtype)
+
+
+def timed(fn, sets, reps):
+    """Mean device time (ms) of one launch: reps x len(sets) back-to-back launches."""
+    for j in range(len(sets)):
+        fn(j)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        for j in range(len(sets)):
+            fn(j)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / (reps * len(sets))
+
+
+def prec_for(dtype, b):
+    if dtype == torch.bfloat16:
+        return "bf16" if b >= 16 else "fp32"
+    return "tf32" if b >= 32 else "fp32"
+
+
+def sweep_c3(out, hbm, bf16_tf, nsets=3, reps=6):
+    layers = [("fc1", 25088, 384, 1536, "aff"), ("fc2", 25088, 1536, 384, "gelu")]
+    rows = []
+    for dtype in (torch.float32, torch.bfloat16):
+        s = 4 if dtype == torch.float32 else 2
+        for lname, M, K, N, fam in layers:
+            Xs = [activation(M, K, fam, SEED + 10 * i + (lname == "fc2"), dtype) for i in range(nsets)]
+            dYs = [grad_out(M, N, SEED + 10 * i + 5, dtype) for i in range(nsets)]
+            for b in (4, 8, 16, 32, 64):
+                nblocks = bp.num_blocks(M, K, b)
+                for keep in (0.1, 0.3, 0.5, 0.7, 0.9, 1.0):
+                    k = bp.keep_count(nblocks, keep)
+                    prec = prec_for(dtype, b)
+                    As = [bp.alloc_bsr(M, K, b, k, dtype, "cuda") for _ in range(nsets)]
+                    dWs = [torch.empty(K, N, device="cuda") for _ in range(nsets)]
+                    Ds = [torch.empty(M, K, dtype=dtype, device="cuda") for _ in range(nsets)]
+                    t_p = timed(lambda j: bp.prune(Xs[j], b, k=k, out=As[j]), Xs, reps)
+                    t_w = timed(lambda j: bp.wgrad(As[j], dYs[j], prec=prec, out=dWs[j]), Xs, reps)
+                    t_d = timed(lambda j: bp.decompress(As[j], out=Ds[j]), Xs, reps)
+                    rp = As[0].rowptr
+                    r_ne = int((rp[1:] > rp[:-1]).sum().item())
+                    ref = Ds[0].double().T @ dYs[0].double()
+                    err = ((dWs[0].double() - ref).norm() / ref.norm().clamp_min(1e-300)).item()
+                    pb = metrics.prune_bytes(M, K, b, k, s)
+                    wb = metrics.wgrad_bytes(M, K, b, k, N, s, s, r_ne)
+                    wf = metrics.wgrad_flops(b, k, N)
+                    db = metrics.decompress_bytes(M, K, b, k, s)
+                    tc_peak = bf16_tf if prec == "bf16" else bf16_tf / 2 if prec == "tf32" else None
+                    w_tf = wf / (t_w * 1e-3) / 1e12
+                    w_gbs = wb / (t_w * 1e-3) / 1e9
+                    roof_t = max(wb / (hbm * 1e9), wf / (tc_peak * 1e12) if tc_peak else 0.0)
+                    row = dict(config="C3", layer=lname, M=M, K=K, N=N, b=b, keep=keep, k=k, dtype=str(dtype)[6:],
+                               prec=prec, prune_ms=t_p, prune_gbs=pb / (t_p * 1e-3) / 1e9,
+                               prune_hbm_frac=pb / (t_p * 1e-3) / 1e9 / hbm, wgrad_ms=t_w, wgrad_tflops=w_tf,
+                               wgrad_gbs=w_gbs, wgrad_tc_frac=(w_tf / tc_peak) if tc_peak else None,
+                               wgrad_roofline_frac=roof_t / (t_w * 1e-3),
+                               wgrad_bound="tensor" if tc_peak and wf / (tc_peak * 1e12) > wb / (hbm * 1e9) else "hbm",
+                               decompress_ms=t_d, decompress_gbs=db / (t_d * 1e-3) / 1e9,
+                               act_bytes_saved=metrics.act_bytes_saved(M, K, b, k, s),
+                               act_saved_frac=metrics.act_bytes_saved(M, K, b, k, s) / (s * M * K),
+                               check_rel_err=err)
+                    rows.append(row)
+                    print(json.dumps(row), flush=True)
+                    out.write(json.dumps(row) + "\n")
+                    del As, dWs, Ds
+            del Xs, dYs
+            torch.cuda.empty_cache()
+    # the whole S12 model: 12 blocks x (fc1 + fc2)
+    model = []
+    for dt in ("float32", "bfloat16"):
+        for b in (4, 8, 16, 32, 64):
+            for keep in (0.1, 0.3, 0.5, 0.7, 0.9, 1.0):
+                sel = [r for r in rows if r["dtype"] == dt and r["b"] == b and r["keep"] == keep]
+                if len(sel) != 2:
+                    continue
+                tot = {x: 12 * sum(r[x] for r in sel) for x in ("prune_ms", "wgrad_ms", "decompress_ms")}
+                m = dict(config="C3-model", model="ResMLP-S12 (12 blocks x fc1+fc2)", dtype=dt, b=b, keep=keep,
+                         **{f"model_{x}": v for x, v in tot.items()},
+                         model_act_bytes_saved=12 * sum(r["act_bytes_saved"] for r in sel))
+                model.append(m)
+                out.write(json.dumps(m) + "\n")
+    return rows, model
+
+
+def sweep_c5(out, hbm, reps=4):
+    K = 1536
+    rows = []
+    for size in (256 << 20, 1 << 30, 4 << 30):
+        M = (size // (K * 4)) // 64 * 64
+        Xs = [activation(M, K, "aff", SEED + 500 + i, torch.float32) for i in range(2)]
+        for b in (4, 16, 32, 64):
+            nblocks = bp.num_blocks(M, K, b)
+            for keep in (0.1, 0.5, 1.0):
+                k = bp.keep_count(nblocks, keep)
+                As = [bp.alloc_bsr(M, K, b, k, torch.float32, "cuda") for _ in range(2)]
+                t_p = timed(lambda j: bp.prune(Xs[j], b, k=k, out=As[j]), Xs, reps)
+                pb = metrics.prune_bytes(M, K, b, k, 4)
+                D = torch.empty(M, K, device="cuda")
+                t_d = timed(lambda j: bp.decompress(As[j], out=D), Xs, reps)
+                db = metrics.decompress_bytes(M, K, b, k, 4)
+                row = dict(config="C5", x_bytes=4 * M * K, M=M, K=K, b=b, keep=keep, k=k, prune_ms=t_p,
+                           prune_gbs=pb / (t_p * 1e-3) / 1e9, prune_hbm_frac=pb / (t_p * 1e-3) / 1e9 / hbm,
+                           decompress_ms=t_d, decompress_gbs=db / (t_d * 1e-3) / 1e9,
+                           decompress_hbm_frac=db / (t_d * 1e-3) / 1e9 / hbm)
+                rows.append(row)
+                print(json.dumps(row), flush=True)
+                out.write(json.dumps(row) + "\n")
+                del As, D
+                torch.cuda.empty_cache()
+        del Xs
+        torch.cuda.empty_cache()
+    return rows
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("which", nargs="+", choices=["c3", "c5"])
+    ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out", "sweep"))
+    a = ap.parse_args()
+    os.makedirs(a.out_dir, exist_ok=True)
+    hbm, bf16_tf, src = peaks()
+    meta = dict(gpu=torch.cuda.get_device_name(0), hbm_gbs=hbm, bf16_tflops=bf16_tf, peak_source=src,
+                when=time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()), lib=bp.version())
+    for w in a.which:
+        with open(os.path.join(a.out_dir, f"{w}.jsonl"), "w") as out:
+            out.write(json.dumps(dict(meta=meta)) + "\n")
+            (sweep_c3 if w == "c3" else sweep_c5)(out, hbm, bf16_tf) if w == "c3" else sweep_c5(out, hbm)
+
+
+if __name__ == "__main__":
+    main()
