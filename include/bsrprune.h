@@ -117,10 +117,11 @@ BSR_API size_t bsr_storage_bytes(int64_t M, int32_t b, int64_t k, int32_t dtype)
 BSR_API size_t bsr_prune_workspace_bytes(int64_t M, int64_t K, int32_t b);
 
 /* Device workspace (bytes) bsr_wgrad needs for this shape and precision.  0
- * means none is needed (a NULL workspace is then accepted).  The tensor-core
- * paths split the block rows over up to 148 CTAs per output tile set and write
- * one partial dW per split there; bsr_wgrad sums them in split order, so the
- * result is deterministic.  Must be 16-byte aligned and must not overlap dW. */
+ * means none is needed (a NULL workspace is then accepted).  Every path
+ * splits the block rows over several CTAs per output tile when the tiles alone
+ * do not fill the GPU (tensor cores: up to 148 CTAs; FP32: up to 2 per SM) and
+ * writes one partial dW per split there; bsr_wgrad sums them in split order, so
+ * the result is deterministic.  Must be 16-byte aligned and must not overlap dW. */
 BSR_API size_t bsr_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec);
 
 /* ---- device work ------------------------------------------------------------ */

@@ -110,7 +110,7 @@ size_t bsr_prune_workspace_bytes(int64_t M, int64_t K, int32_t b) {
 
 size_t bsr_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec) {
     if (bsr_num_blocks(M, K, b) < 0 || N <= 0) return 0;
-    if (prec == BSR_PREC_FP32) return 0;
+    if (prec == BSR_PREC_FP32) return bsrp::wgrad_simt_ws_bytes(M, K, b, N);
     return bsrp::wgrad_tc_ws_bytes(M, K, b, N);
 }
 
@@ -199,10 +199,17 @@ bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t
         return fail(BSR_ERR_INVALID_ARG, "dW overlaps dY");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (prec) {
-        case BSR_PREC_FP32:
-            return cuda_status(bsrp::launch_wgrad_simt(A->rowptr, A->colidx, A->values, esx, A->M, A->K, A->b, dY,
-                                                       esy, N, dW, accumulate, s),
+        case BSR_PREC_FP32: {
+            const size_t need = bsrp::wgrad_simt_ws_bytes(A->M, A->K, A->b, N);
+            if (need && (!ws || ws_bytes < need))
+                return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+            if (need && !aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
+            if (need && overlap(ws, need, dW, (size_t)A->K * N * 4))
+                return fail(BSR_ERR_INVALID_ARG, "workspace overlaps dW");
+            return cuda_status(bsrp::launch_wgrad_simt(A->rowptr, A->colidx, A->nnzb ? A->values : nullptr, esx, A->M,
+                                                       A->K, A->b, dY, esy, N, dW, accumulate, ws, s),
                                "bsr_wgrad (fp32) launch");
+        }
         case BSR_PREC_TF32:
         case BSR_PREC_BF16: {
             const int want = prec == BSR_PREC_TF32 ? BSR_DT_F32 : BSR_DT_BF16;

@@ -25,10 +25,11 @@ cudaError_t launch_block_sumsq(const void *X, int64_t M, int64_t K, int b, int e
 cudaError_t launch_decompress(const int32_t *rowptr, const int32_t *colidx, const void *values,
                               int64_t M, int64_t K, int b, int es, void *Xout, cudaStream_t stream);
 
-// dW = X_bsr^T dY, fp32 SIMT path (deterministic).
+// dW = X_bsr^T dY, fp32 SIMT path (deterministic); split-K partials in ws.
+size_t wgrad_simt_ws_bytes(int64_t M, int64_t K, int b, int64_t N);
 cudaError_t launch_wgrad_simt(const int32_t *rowptr, const int32_t *colidx, const void *values,
                               int es_x, int64_t M, int64_t K, int b, const void *dY, int es_y,
-                              int64_t N, float *dW, int accumulate, cudaStream_t stream);
+                              int64_t N, float *dW, int accumulate, void *ws, cudaStream_t stream);
 
 // dW = X_bsr^T dY on tcgen05 tensor cores.  kind: 0 = tf32 (fp32 operands),
 // 1 = f16 (bf16 operands).

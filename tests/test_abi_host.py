@@ -71,7 +71,9 @@ def test_storage_bytes_matches_oracle(lib, M, b, k):
 def test_workspace_query(lib):
     assert lib.bsr_prune_workspace_bytes(256, 256, 16) >= 2 * 256 * 4
     assert lib.bsr_prune_workspace_bytes(100, 256, 16) == 0
-    assert lib.bsr_wgrad_workspace_bytes(256, 256, 16, 256, 0) == 0
+    # FP32 path: one 128 x 128 tile set, 16 block rows -> 2 splits of partial dW
+    assert lib.bsr_wgrad_workspace_bytes(256, 256, 16, 256, 0) == 2 * 256 * 256 * 4
+    assert lib.bsr_wgrad_workspace_bytes(16, 256, 16, 256, 0) == 0  # one block row: no split
 
 
 # ------------------------------------------------------------ validation errors
