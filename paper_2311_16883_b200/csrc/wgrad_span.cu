@@ -375,7 +375,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tm_v2, const __grid_constant__ CUtensorMap tm_v4,
                       const __grid_constant__ CUtensorMap tm_v8, Params p) {
     using C = Cfg<KIND, B>;
-    constexpr uint32_t kFullArrivals = 1 + 4 * CG;
+    // full-barrier arrivals per phase: the producer (+ dY bytes), the 128 loader threads'
+    // cp.async completions, and for a pair the peer's relay
+    constexpr uint32_t kFullArrivals = 1 + 128 + (CG == 2 ? 1 : 0);
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = p.stages;
@@ -387,6 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *plan_full = reinterpret_cast<uint64_t *>(s_meta + kMaxStages);  // [2]
     uint64_t *plan_empty = plan_full + 2;                                      // [2]
     uint32_t *s_cnt = reinterpret_cast<uint32_t *>(plan_empty + 2);            // [2] records per plan group
+    uint64_t *xfull = reinterpret_cast<uint64_t *>(s_cnt + 2);                  // [kMaxStages] peer: loaders done
     uint4 *s_plan = reinterpret_cast<uint4 *>(smem + (size_t)S * p.stage_bytes + kBarBytes);  // [2][32]
     int32_t *s_rp = reinterpret_cast<int32_t *>(s_plan + 2 * 32);                // [33]
     uint16_t *s_col = reinterpret_cast<uint16_t *>(s_rp + 36);                  // [kColCap]
@@ -414,10 +417,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v8)) : "memory");
         for (int i = 0; i < 2; ++i) {
             mbar_init(plan_full + i, 1);
-            mbar_init(plan_empty + i, 5);  // the producer warp and the four loader warps
+            mbar_init(plan_empty + i, CG == 2 && rank != 0 ? 6 : 5);  // producer, 4 loader warps (+ peer relay)
         }
         for (int s = 0; s < S; ++s) {
-            mbar_init(full + s, kFullArrivals);  // producer (+ dY TMA bytes) + the loader warps of both CTAs
+            mbar_init(full + s, kFullArrivals);  // producer (+ dY TMA bytes), loader threads, peer relay
+            mbar_init(xfull + s, 128);           // peer CTA: its loader threads' cp.async completions
             mbar_init(empty + s, 1);  // one MMA commit
         }
         mbar_init(accfull, 1);
@@ -633,37 +637,48 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             mma_commit<CG>(accfull);
         }
+    } else if (CG == 2 && warp == 2 && rank != 0) {
+        // ------------------------------------------------ peer relay
+        // cp.async completions can only arrive on a CTA-local barrier: once the
+        // peer's loaders' copies of a row have landed (xfull), one arrival on the
+        // leader's full barrier of that stage, over the cluster.
+        uint32_t full_leader = smem_u32(full);
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(full_leader) : "r"(full_leader));
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int g = 0;; ++g) {
+            const int buf = g & 1;
+            mbar_wait_sleep(plan_full + buf, (g >> 1) & 1);
+            const uint32_t cnt = s_cnt[buf];
+            if (cnt == kSentinel) break;
+            for (uint32_t r = 0; r < cnt; ++r) {
+                mbar_wait(xfull + stage, phase, 5, (uint32_t)stage);
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                     full_leader + (uint32_t)stage * 8u)
+                                 : "memory");
+                __syncwarp();
+                if (++stage == S) { stage = 0; phase ^= 1u; }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(plan_empty + buf);
+        }
     } else if (warp >= 4) {
         // ------------------------------------------------ X-block loaders (then the epilogue)
         // The same plan sequence as the producer.  Each block row's share of its
         // spans is copied global -> shared with 16-byte cp.async (pruned blocks:
-        // src-size 0, i.e. zero fill) straight into the swizzled UMMA image: the
-        // TMA engine only streams dY.  Completion: cp.async groups, LAG rows
-        // behind; then a proxy fence and one arrival per warp on the stage's full
-        // barrier (the leader's, over the cluster, for the peer CTA).
+        // src-size 0, i.e. zero fill) straight into the swizzled UMMA image, on
+        // the LSU path, while the TMA engine streams dY.  Every loader thread then
+        // arms cp.async.mbarrier.arrive on the stage's full barrier (the peer CTA:
+        // on its local xfull barrier, relayed to the leader by warp 2), so the
+        // barrier completes when the copies land -- no waiting here.
         {
-            constexpr int LAG = 2;
             constexpr int PPB = C::BLOCK_BYTES / 16;  // 16-byte pieces per block
             const int tid = threadIdx.x - 128;
             const int cb = p.cb, cbh = p.cb / CG;
-            int stage = 0, rstage[LAG + 1];
+            int stage = 0;
             uint32_t phase = 0;
-            int issued = 0;
-            uint32_t full_addr0 = smem_u32(full);
-            if (CG == 2 && rank != 0)
-                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(full_addr0) : "r"(full_addr0));
-            auto retire = [&](int st) {  // copies of the row in stage st have landed
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) {
-                    if (CG == 2 && rank != 0)
-                        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                                         full_addr0 + (uint32_t)st * 8u)
-                                     : "memory");
-                    else
-                        mbar_arrive(full + st);
-                }
-            };
+            uint64_t *arrive_bar = (CG == 2 && rank != 0) ? xfull : full;
             for (int g = 0;; ++g) {
                 const int buf = g & 1;
                 mbar_wait_sleep(plan_full + buf, (g >> 1) & 1);
@@ -677,37 +692,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(empty + stage, phase ^ 1u, 4, (uint32_t)stage);
                     const uint32_t xb = smem0 + (uint32_t)stage * p.stage_bytes + C::SLAB;
                     const int h0 = sp.len[0] / CG, h1 = sp.len[1] / CG;
-                    const int total = (h0 + h1) * PPB;
-                    if (!(SPAN_MODE & 2)) {
-                        for (int q = tid; q < total; q += 128) {
-                            const int blk = q / PPB, off = q % PPB;
-                            const int c = blk >= h0;
-                            const int j = blk - (c ? h0 : 0);
-                            const int J = c * cb + sp.f[c] + (int)rank * (c ? h1 : h0) + j;
-                            const bool kept = J < nbJ && ((mk >> J) & 1u);
-                            const int idx = kept ? bs + __popc(mk & ((1u << J) - 1u)) : 0;
-                            const uint8_t *src = p.values + (int64_t)idx * C::BLOCK_BYTES + off * 16;
-                            const uint32_t dst = xb + (uint32_t)((c * cbh + j) * C::BLOCK_BYTES) +
-                                                 block_smem_off<KIND, B>((uint32_t)off * 16u);
-                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                                         "r"(kept ? 16 : 0)
-                                         : "memory");
-                        }
+                    const int total = (SPAN_MODE & 2) ? 0 : (h0 + h1) * PPB;
+                    for (int q = tid; q < total; q += 128) {
+                        const int blk = q / PPB, off = q % PPB;
+                        const int c = blk >= h0;
+                        const int j = blk - (c ? h0 : 0);
+                        const int J = c * cb + sp.f[c] + (int)rank * (c ? h1 : h0) + j;
+                        const bool kept = J < nbJ && ((mk >> J) & 1u);
+                        const int idx = kept ? bs + __popc(mk & ((1u << J) - 1u)) : 0;
+                        const uint8_t *src = p.values + (int64_t)idx * C::BLOCK_BYTES + off * 16;
+                        const uint32_t dst = xb + (uint32_t)((c * cbh + j) * C::BLOCK_BYTES) +
+                                             block_smem_off<KIND, B>((uint32_t)off * 16u);
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                                     "r"(kept ? 16 : 0)
+                                     : "memory");
                     }
-                    asm volatile("cp.async.commit_group;" ::: "memory");
-                    rstage[issued % (LAG + 1)] = stage;
-                    ++issued;
-                    if (issued > LAG) {
-                        asm volatile("cp.async.wait_group %0;" ::"n"(LAG) : "memory");
-                        retire(rstage[(issued - 1 - LAG) % (LAG + 1)]);
-                    }
+                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(arrive_bar + stage))
+                                 : "memory");
                     if (++stage == S) { stage = 0; phase ^= 1u; }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(plan_empty + buf);
             }
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            for (int i = max(0, issued - LAG); i < issued; ++i) retire(rstage[i % (LAG + 1)]);
         }
         // ------------------------------------------------ epilogue
         mbar_wait_sleep(accfull, 0);
