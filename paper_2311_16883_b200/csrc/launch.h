@@ -11,7 +11,7 @@ void count_launch(uint64_t n = 1);
 
 // Workspace layout of bsr_prune (byte offsets; all 256-aligned).
 struct PruneWs {
-    size_t hdr, hist1, hist2, hist3, cta_cnt, sumsq, slot, total, zero_bytes;
+    size_t hdr, hist1, hist2, hist3, cta_cnt, sumsq, slot, cand, total, zero_bytes;
 };
 constexpr int kMaxGrid = 2048;
 PruneWs prune_ws_layout(int64_t N);

@@ -41,6 +41,7 @@ namespace bsrp {
 
 constexpr int kThreads = 512;
 constexpr int kH1 = 4096, kH2 = 1024, kH3 = 512;  // digit sizes: key bits 30..19, 18..9, 8..0
+constexpr int kCandMax = kH1;  // boundary-bin candidates exchanged through the workspace
 
 struct PruneParams {
     const void *X;
@@ -50,6 +51,7 @@ struct PruneParams {
     float *sumsq;
     int32_t *slot;
     uint32_t *bar, *hist1, *hist2, *hist3, *cta_cnt;
+    uint2 *cand;  // [kCandMax] (key, flat index) of the boundary bin's blocks
 };
 
 // Selection key of a block: fp32 bits of sumsq (>= 0, so the integer order is
@@ -242,8 +244,9 @@ __device__ unsigned long long g_ptrace[2048][8];
 template <int ES, int B>
 __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
     using G_ = Geo<ES, B>;
-    using V = typename G_::V;
-    __shared__ uint32_t s_hist[kH1];
+    __shared__ uint32_t s_hist[kH1];  // level-1 histogram, then the candidate keys
+    __shared__ uint32_t s_f[kCandMax];  // candidate flat indices
+    __shared__ uint32_t s_h2[1024];     // candidate refinement histogram
     __shared__ uint64_t s_warp[32];
     __shared__ uint32_t s_sel[4];
 
@@ -283,66 +286,171 @@ __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
     uint32_t prefix = s_sel[0], above = s_sel[1], bincnt = s_sel[2];
     int shift = 19;
     uint32_t r = k - above;
-    if (r < bincnt) {  // boundary bin is split: refine on key bits 18..9
-        for (int i = threadIdx.x; i < kH2; i += kThreads) s_hist[i] = 0;
-        __syncthreads();
+    uint64_t pre = 0;
+    bool have_pre = false;
+    if (r < bincnt) {
+        // Candidate exchange (one barrier instead of two refinement rounds and the
+        // scan barrier): every CTA publishes its count of keys above the boundary
+        // bin and appends its keys inside the bin, with their flat index, to a
+        // global list.  After the barrier each CTA resolves the exact threshold
+        // from the list and its own prefix counts (CTAs before it + listed keys
+        // before its range), unless the bin overflowed the list.
+        const uint32_t prefix1 = prefix;
+        // pass A: this CTA's counts (keys above the bin, keys in it) -> one atomic
+        // reservation of list slots per CTA (a single hot counter would serialise)
+        uint32_t na = 0, ni = 0;
         for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
-            uint32_t key = key_of(p.sumsq[f]);
-            if ((key >> 19) == prefix) atomicAdd(&s_hist[(key >> 9) & (kH2 - 1)], 1u);
+            const uint32_t hb = key_of(p.sumsq[f]) >> 19;
+            na += hb > prefix1;
+            ni += hb == prefix1;
         }
-        __syncthreads();
-        for (int i = threadIdx.x; i < kH2; i += kThreads)
-            if (s_hist[i]) atomicAdd(p.hist2 + i, s_hist[i]);
+        uint32_t slot0, ni_cta;
+        {
+            uint64_t tot;
+            block_excl_scan(((uint64_t)na << 32) | ni, s_warp, tot);
+            ni_cta = (uint32_t)tot;
+            if (threadIdx.x == 0) {
+                p.cta_cnt[2 * blockIdx.x] = (uint32_t)(tot >> 32);
+                s_sel[3] = (uint32_t)tot ? atomicAdd(p.bar + 16, (uint32_t)tot) : 0u;
+            }
+            __syncthreads();
+            slot0 = s_sel[3];
+        }
+        // pass B: append the bin's keys with their flat index, in flat order
+        for (int64_t fb = f0; fb < f1 && ni_cta; fb += kThreads) {
+            const int64_t f = fb + threadIdx.x;
+            uint32_t key = 0;
+            bool in = false;
+            if (f < f1) {
+                key = key_of(p.sumsq[f]);
+                in = (key >> 19) == prefix1;
+            }
+            uint64_t tot;
+            const uint32_t ex = (uint32_t)block_excl_scan(in ? 1u : 0u, s_warp, tot);
+            const uint32_t slot = slot0 + ex;
+            if (in && slot < (uint32_t)kCandMax) p.cand[slot] = make_uint2(key, (uint32_t)f);
+            slot0 += (uint32_t)tot;
+        }
         grid_barrier(p.bar, nbar++);
-        select_bin(p.hist2, kH2, r, s_warp, s_sel);
-        prefix = (prefix << 10) | s_sel[0];
-        above += s_sel[1];
-        bincnt = s_sel[2];
-        shift = 9;
-        r = k - above;
-        if (r < bincnt) {  // refine on key bits 8..0
-            for (int i = threadIdx.x; i < kH3; i += kThreads) s_hist[i] = 0;
+        PTRACE(6);
+        const uint32_t nc = __ldcg(p.bar + 16);
+        if (nc <= (uint32_t)kCandMax) {
+            for (uint32_t i0 = threadIdx.x; i0 < nc; i0 += 8 * kThreads) {  // 8 independent loads in flight
+                uint2 c[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) c[u] = i0 + u * kThreads < nc ? __ldcg(p.cand + i0 + u * kThreads) : uint2{};
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (i0 + u * kThreads < nc) {
+                        s_hist[i0 + u * kThreads] = c[u].x;
+                        s_f[i0 + u * kThreads] = c[u].y;
+                    }
+            }
+            __syncthreads();
+            for (int pass = 0; pass < 2 && r < bincnt; ++pass) {  // key bits 18..9, then 8..0
+                const int w = pass == 0 ? 10 : 9;
+                const int nshift = shift - w;
+                for (int i = threadIdx.x; i < (1 << w); i += kThreads) s_h2[i] = 0;
+                __syncthreads();
+                for (uint32_t ib = 0; ib < nc; ib += kThreads) {
+                    const uint32_t i = ib + threadIdx.x;
+                    const uint32_t key = i < nc ? s_hist[i] : 0u;
+                    const bool in = i < nc && (key >> shift) == prefix;
+                    const uint32_t bin = (key >> nshift) & ((1u << w) - 1u);
+                    const uint32_t im = __ballot_sync(0xffffffffu, in);
+                    if (!im) continue;
+                    const int l0 = __ffs(im) - 1;
+                    const uint32_t b0 = __shfl_sync(0xffffffffu, bin, l0);
+                    if (__all_sync(0xffffffffu, !in || bin == b0)) {  // a warp of ties adds once
+                        if (lane == l0) atomicAdd(&s_h2[b0], (uint32_t)__popc(im));
+                    } else if (in) {
+                        atomicAdd(&s_h2[bin], 1u);
+                    }
+                }
+                __syncthreads();
+                select_bin<false>(s_h2, 1 << w, r, s_warp, s_sel);
+                prefix = (prefix << w) | s_sel[0];
+                above += s_sel[1];
+                bincnt = s_sel[2];
+                shift = nshift;
+                r = k - above;
+            }
+            PTRACE(7);
+            // (above, tie) counts of every block before this CTA's range
+            uint64_t cnt = 0;
+            for (int c = threadIdx.x; c < (int)blockIdx.x; c += kThreads) cnt += (uint64_t)__ldcg(p.cta_cnt + 2 * c) << 32;
+            for (uint32_t i = threadIdx.x; i < nc; i += kThreads) {
+                if ((int64_t)s_f[i] >= f0) continue;
+                const uint32_t kk = s_hist[i] >> shift;
+                cnt += kk > prefix ? (uint64_t)1 << 32 : (kk == prefix ? 1u : 0u);
+            }
+            uint64_t tot;
+            block_excl_scan(cnt, s_warp, tot);
+            pre = tot;
+            have_pre = true;
+        } else {
+            // the boundary bin overflowed the list (heavy ties): global refinement rounds
+            for (int i = threadIdx.x; i < kH2; i += kThreads) s_hist[i] = 0;
             __syncthreads();
             for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
                 uint32_t key = key_of(p.sumsq[f]);
-                if ((key >> 9) == prefix) atomicAdd(&s_hist[key & (kH3 - 1)], 1u);
+                if ((key >> 19) == prefix) atomicAdd(&s_hist[(key >> 9) & (kH2 - 1)], 1u);
             }
             __syncthreads();
-            for (int i = threadIdx.x; i < kH3; i += kThreads)
-                if (s_hist[i]) atomicAdd(p.hist3 + i, s_hist[i]);
+            for (int i = threadIdx.x; i < kH2; i += kThreads)
+                if (s_hist[i]) atomicAdd(p.hist2 + i, s_hist[i]);
             grid_barrier(p.bar, nbar++);
-            select_bin(p.hist3, kH3, r, s_warp, s_sel);
-            prefix = (prefix << 9) | s_sel[0];
+            select_bin(p.hist2, kH2, r, s_warp, s_sel);
+            prefix = (prefix << 10) | s_sel[0];
             above += s_sel[1];
-            shift = 0;
+            bincnt = s_sel[2];
+            shift = 9;
             r = k - above;
+            if (r < bincnt) {  // refine on key bits 8..0
+                for (int i = threadIdx.x; i < kH3; i += kThreads) s_hist[i] = 0;
+                __syncthreads();
+                for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
+                    uint32_t key = key_of(p.sumsq[f]);
+                    if ((key >> 9) == prefix) atomicAdd(&s_hist[key & (kH3 - 1)], 1u);
+                }
+                __syncthreads();
+                for (int i = threadIdx.x; i < kH3; i += kThreads)
+                    if (s_hist[i]) atomicAdd(p.hist3 + i, s_hist[i]);
+                grid_barrier(p.bar, nbar++);
+                select_bin(p.hist3, kH3, r, s_warp, s_sel);
+                prefix = (prefix << 9) | s_sel[0];
+                above += s_sel[1];
+                shift = 0;
+                r = k - above;
+            }
         }
     }
 
     PTRACE(3);
     // ---------------- phase 3: flat-order scan -> slots, colidx, rowptr
-    uint32_t na = 0, nt = 0;
-    for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
-        uint32_t kk = key_of(p.sumsq[f]) >> shift;
-        na += kk > prefix;
-        nt += kk == prefix;
-    }
-    {
-        uint64_t tot;
-        block_excl_scan(((uint64_t)na << 32) | nt, s_warp, tot);
-        if (threadIdx.x == 0) {
-            p.cta_cnt[2 * blockIdx.x] = (uint32_t)(tot >> 32);
-            p.cta_cnt[2 * blockIdx.x + 1] = (uint32_t)tot;
+    if (!have_pre) {
+        uint32_t na = 0, nt = 0;
+        for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
+            uint32_t kk = key_of(p.sumsq[f]) >> shift;
+            na += kk > prefix;
+            nt += kk == prefix;
         }
-    }
-    grid_barrier(p.bar, nbar++);
-    uint64_t pre = 0;
-    for (int c = threadIdx.x; c < (int)blockIdx.x; c += kThreads)
-        pre += ((uint64_t)__ldcg(p.cta_cnt + 2 * c) << 32) | __ldcg(p.cta_cnt + 2 * c + 1);
-    {
-        uint64_t tot;
-        block_excl_scan(pre, s_warp, tot);
-        pre = tot;
+        {
+            uint64_t tot;
+            block_excl_scan(((uint64_t)na << 32) | nt, s_warp, tot);
+            if (threadIdx.x == 0) {
+                p.cta_cnt[2 * blockIdx.x] = (uint32_t)(tot >> 32);
+                p.cta_cnt[2 * blockIdx.x + 1] = (uint32_t)tot;
+            }
+        }
+        grid_barrier(p.bar, nbar++);
+        for (int c = threadIdx.x; c < (int)blockIdx.x; c += kThreads)
+            pre += ((uint64_t)__ldcg(p.cta_cnt + 2 * c) << 32) | __ldcg(p.cta_cnt + 2 * c + 1);
+        {
+            uint64_t tot;
+            block_excl_scan(pre, s_warp, tot);
+            pre = tot;
+        }
     }
     // Self-cleaning workspace: every CTA is past its last read of the barrier counter
     // and the histograms; the last one to get here zeroes them for the next launch
@@ -359,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
         for (int i = threadIdx.x; i < kH3; i += kThreads) p.hist3[i] = 0;
         if (threadIdx.x == 0) {
             p.bar[0] = 0;
+            p.bar[16] = 0;
             p.bar[32] = 0;
         }
     }
@@ -637,6 +746,7 @@ PruneWs prune_ws_layout(int64_t N) {
     w.cta_cnt = o;  o += align256(2 * kMaxGrid * 4);
     w.sumsq = o;    o += align256((size_t)N * 4);
     w.slot = o;     o += align256((size_t)N * 4);
+    w.cand = o;     o += align256((size_t)kCandMax * 8);
     w.total = o;
     return w;
 }
@@ -736,6 +846,7 @@ cudaError_t launch_prune(const void *X, int64_t M, int64_t K, int b, int es, int
     p.cta_cnt = reinterpret_cast<uint32_t *>(base + w.cta_cnt);
     p.sumsq = reinterpret_cast<float *>(base + w.sumsq);
     p.slot = reinterpret_cast<int32_t *>(base + w.slot);
+    p.cand = reinterpret_cast<uint2 *>(base + w.cand);
 #define CALL(ES_, B_) (p.upr = units_per_row<ES_, B_>(p.nbc), p.units = p.nbr * p.upr, \
                        launch_prune_t<ES_, B_>(p, stream, ws, w))
     if (es == 4) {

@@ -30,7 +30,7 @@ int main(int argc, char **argv) {
     for (int c = 0; c < 2048; ++c) if (tr[c][0]) { t0 = std::min(t0, tr[c][0]); ++nC; }
     double mx[6] = {0};
     for (int c = 0; c < nC; ++c) for (int i = 0; i < 6; ++i) mx[i] = std::max(mx[i], (tr[c][i] - t0) / 1e3);
-    { double a6=0,a7=0; for (int c = 0; c < nC; ++c) { a6 = std::max(a6, (tr[c][6]-t0)/1e3); a7 = std::max(a7, (tr[c][7]-t0)/1e3);} printf("keys loaded %.2f cands %.2f\n", a6, a7); }
+    { double a6=0,a7=0; for (int c = 0; c < nC; ++c) { a6 = std::max(a6, (tr[c][6]-t0)/1e3); a7 = std::max(a7, (tr[c][7]-t0)/1e3);} printf("barrier2/keys %.2f cands-refined %.2f\n", a6, a7); }
     printf("CTAs %d; max over CTAs: start %.2f  p1 done %.2f  barrier1 %.2f  select done %.2f  scan done %.2f  pack done %.2f\n", nC, mx[0], mx[1], mx[2], mx[3], mx[4], mx[5]);
     for (int c : {0, nC - 1}) printf("CTA %d: %.2f %.2f %.2f %.2f %.2f %.2f\n", c, (tr[c][0]-t0)/1e3, (tr[c][1]-t0)/1e3, (tr[c][2]-t0)/1e3, (tr[c][3]-t0)/1e3, (tr[c][4]-t0)/1e3, (tr[c][5]-t0)/1e3);
     return 0;
