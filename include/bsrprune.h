@@ -168,6 +168,37 @@ BSR_API bsr_status_t bsr_decompress(const bsr_t *A, void *X_out, void *stream);
 BSR_API bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dW,
                        int32_t accumulate, int32_t prec, void *ws, size_t ws_bytes, void *stream);
 
+/* ---- cross-rank global top-k ----------------------------
+ * Under data parallelism each rank holds a shard of X's rows.  bsr_prune keeps
+ * keep*N_rank blocks per rank (per-rank scope, R2).  These three calls
+ * let the caller keep the k = bsr_keep_count(N_total, keep) largest blocks of the
+ * CONCATENATED X instead (rank order = flat order; ties: lower rank, then lower
+ * flat index first), so multi-GPU selection equals the single-GPU one
+ * (P:L413-418 over the whole batch).  The library does not communicate: the
+ * caller all-reduces the digit histograms and all-gathers the counts between
+ * the calls (paper_2311_16883_b200.prune_global).  Keys are the fp32 bit
+ * patterns of the block sums of squares (bit 31 cleared), exactly as bsr_prune.
+ * `ws` is the bsr_prune workspace (same size, zero-filled on first use).
+ *
+ * bsr_select_hist: level 0 computes every block's sum of squares into ws and
+ *   hist[4096] = histogram of key bits 30..19; level 1: hist[1024] of bits 18..9
+ *   of the keys whose bits 30..19 == prefix; level 2: hist[512] of bits 8..0 of
+ *   the keys whose bits 30..9 == prefix.  hist: device uint32, zeroed by the call.
+ * bsr_select_counts: counts[0] = #blocks with (key >> shift) > threshold,
+ *   counts[1] = #blocks with (key >> shift) == threshold (device uint64[2]).
+ * bsr_prune_threshold: pack the blocks with (key >> shift) > threshold plus the
+ *   first tie_take blocks with (key >> shift) == threshold in flat order into
+ *   `out` (layout as bsr_prune); k must equal counts[0] + tie_take of the same
+ *   (threshold, shift), out sized for k.  Needs the level-0 sums in ws. */
+BSR_API bsr_status_t bsr_select_hist(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype, int32_t level,
+                                     uint32_t prefix, uint32_t *hist, void *ws, size_t ws_bytes, void *stream);
+BSR_API bsr_status_t bsr_select_counts(int64_t M, int64_t K, int32_t b, uint32_t threshold, int32_t shift,
+                                       uint64_t *counts, void *ws, size_t ws_bytes, void *stream);
+BSR_API bsr_status_t bsr_prune_threshold(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype,
+                                         uint32_t threshold, int32_t shift, int64_t tie_take, int64_t k, bsr_t *out,
+                                         void *ws, size_t ws_bytes, void *stream);
+
+
 /* Static description of a status code. */
 BSR_API const char *bsr_status_string(int32_t status);
 

@@ -20,7 +20,7 @@ PREC = {"fp32": 0, "tf32": 1, "bf16": 2}
 
 EXPORTED = ["bsr_num_blocks", "bsr_keep_count", "bsr_storage_bytes", "bsr_prune_workspace_bytes",
             "bsr_wgrad_workspace_bytes", "bsr_prune", "bsr_prune_k", "bsr_block_sumsq", "bsr_decompress",
-            "bsr_wgrad", "bsr_status_string", "bsr_last_error", "bsr_kernel_launches", "bsr_version"]
+            "bsr_wgrad", "bsr_select_hist", "bsr_select_counts", "bsr_prune_threshold", "bsr_status_string", "bsr_last_error", "bsr_kernel_launches", "bsr_version"]
 
 
 class BsrT(ctypes.Structure):
@@ -61,6 +61,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "bsr_block_sumsq": (i32, [vp, i64, i64, i32, i32, vp, vp]),
         "bsr_decompress": (i32, [P, vp, vp]),
         "bsr_wgrad": (i32, [P, vp, i32, i64, vp, i32, i32, vp, sz, vp]),
+        "bsr_select_hist": (i32, [vp, i64, i64, i32, i32, i32, ctypes.c_uint32, vp, vp, sz, vp]),
+        "bsr_select_counts": (i32, [i64, i64, i32, ctypes.c_uint32, i32, vp, vp, sz, vp]),
+        "bsr_prune_threshold": (i32, [vp, i64, i64, i32, i32, ctypes.c_uint32, i32, i64, i64, P, vp, sz, vp]),
         "bsr_status_string": (ctypes.c_char_p, [i32]),
         "bsr_last_error": (ctypes.c_char_p, []),
         "bsr_kernel_launches": (ctypes.c_uint64, []),

@@ -172,6 +172,72 @@ bsr_status_t bsr_block_sumsq(const void *X, int64_t M, int64_t K, int32_t b, int
                        "bsr_block_sumsq launch");
 }
 
+/* ---- cross-rank global top-k (select_global.cu) ---- */
+static bsr_status_t check_ws(int64_t N, void *ws, size_t ws_bytes) {
+    const size_t need = bsrp::prune_ws_layout(N).total;
+    if (!ws || ws_bytes < need)
+        return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+    if (!aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
+    return BSR_OK;
+}
+
+bsr_status_t bsr_select_hist(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype, int32_t level,
+                             uint32_t prefix, uint32_t *hist, void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_shape(M, K, b, dtype);
+    if (st != BSR_OK) return st;
+    if (level < 0 || level > 2) return fail(BSR_ERR_INVALID_ARG, "level=%d must be 0, 1 or 2", level);
+    if (!hist) return fail(BSR_ERR_INVALID_ARG, "hist is NULL");
+    if (level == 0 && !X) return fail(BSR_ERR_INVALID_ARG, "X is NULL");
+    if (level == 0 && !aligned16(X)) return fail(BSR_ERR_ALIGNMENT, "X is not 16-byte aligned");
+    st = check_ws((M / b) * (K / b), ws, ws_bytes);
+    if (st != BSR_OK) return st;
+    return cuda_status(bsrp::launch_select_hist(X, M, K, b, elem_size(dtype), level, prefix, hist, ws,
+                                                static_cast<cudaStream_t>(stream)),
+                       "bsr_select_hist launch");
+}
+
+bsr_status_t bsr_select_counts(int64_t M, int64_t K, int32_t b, uint32_t threshold, int32_t shift, uint64_t *counts,
+                               void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_shape(M, K, b, BSR_DT_F32);
+    if (st != BSR_OK) return st;
+    if (shift != 0 && shift != 9 && shift != 19) return fail(BSR_ERR_INVALID_ARG, "shift=%d must be 0, 9 or 19", shift);
+    if (!counts) return fail(BSR_ERR_INVALID_ARG, "counts is NULL");
+    st = check_ws((M / b) * (K / b), ws, ws_bytes);
+    if (st != BSR_OK) return st;
+    return cuda_status(bsrp::launch_select_counts(M, K, b, threshold, shift, counts, ws,
+                                                  static_cast<cudaStream_t>(stream)),
+                       "bsr_select_counts launch");
+}
+
+bsr_status_t bsr_prune_threshold(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype, uint32_t threshold,
+                                 int32_t shift, int64_t tie_take, int64_t k, bsr_t *out, void *ws, size_t ws_bytes,
+                                 void *stream) {
+    bsr_status_t st = check_shape(M, K, b, dtype);
+    if (st != BSR_OK) return st;
+    const int64_t N = (M / b) * (K / b);
+    if (shift != 0 && shift != 9 && shift != 19) return fail(BSR_ERR_INVALID_ARG, "shift=%d must be 0, 9 or 19", shift);
+    if (k < 0 || k > N) return fail(BSR_ERR_INVALID_ARG, "k=%lld outside [0, N=%lld]", (long long)k, (long long)N);
+    if (tie_take < 0 || tie_take > k) return fail(BSR_ERR_INVALID_ARG, "tie_take=%lld outside [0, k]", (long long)tie_take);
+    if (!X) return fail(BSR_ERR_INVALID_ARG, "X is NULL");
+    if (!out || !out->rowptr) return fail(BSR_ERR_INVALID_ARG, "output BSR descriptor / rowptr is NULL");
+    if (k > 0 && (!out->colidx || !out->values))
+        return fail(BSR_ERR_INVALID_ARG, "out->colidx / out->values are NULL with k=%lld", (long long)k);
+    if (!aligned16(X)) return fail(BSR_ERR_ALIGNMENT, "X is not 16-byte aligned");
+    if (k > 0 && !aligned16(out->values)) return fail(BSR_ERR_ALIGNMENT, "out->values is not 16-byte aligned");
+    st = check_ws(N, ws, ws_bytes);
+    if (st != BSR_OK) return st;
+    cudaError_t e = bsrp::launch_prune_threshold(X, M, K, b, elem_size(dtype), threshold, shift, (uint32_t)tie_take, k,
+                                                 out->rowptr, out->colidx, out->values, ws,
+                                                 static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_status(e, "bsr_prune_threshold launch");
+    out->M = M;
+    out->K = K;
+    out->b = b;
+    out->dtype = dtype;
+    out->nnzb = k;
+    return ok();
+}
+
 bsr_status_t bsr_decompress(const bsr_t *A, void *X_out, void *stream) {
     bsr_status_t st = check_bsr(A);
     if (st != BSR_OK) return st;

@@ -25,6 +25,15 @@ cudaError_t launch_block_sumsq(const void *X, int64_t M, int64_t K, int b, int e
 cudaError_t launch_decompress(const int32_t *rowptr, const int32_t *colidx, const void *values,
                               int64_t M, int64_t K, int b, int es, void *Xout, cudaStream_t stream);
 
+// Cross-rank global top-k steps (select_global.cu, prune.cu).
+cudaError_t launch_select_hist(const void *X, int64_t M, int64_t K, int b, int es, int level, uint32_t prefix,
+                               uint32_t *hist, void *ws, cudaStream_t stream);
+cudaError_t launch_select_counts(int64_t M, int64_t K, int b, uint32_t T, int shift, uint64_t *counts, void *ws,
+                                 cudaStream_t stream);
+cudaError_t launch_prune_threshold(const void *X, int64_t M, int64_t K, int b, int es, uint32_t T, int shift,
+                                   uint32_t tie_take, int64_t k, int32_t *rowptr, int32_t *colidx, void *values,
+                                   void *ws, cudaStream_t stream);
+
 // dW = X_bsr^T dY, fp32 SIMT path (deterministic); split-K partials in ws.
 size_t wgrad_simt_ws_bytes(int64_t M, int64_t K, int b, int64_t N);
 cudaError_t launch_wgrad_simt(const int32_t *rowptr, const int32_t *colidx, const void *values,

@@ -193,8 +193,8 @@ __device__ __forceinline__ void scan_and_index(const PruneParams &p, int64_t f0,
         uint64_t ex = block_excl_scan(((uint64_t)a << 32) | t, s_warp, tot);
         const uint32_t ab = base_a + (uint32_t)(ex >> 32), tb = base_t + (uint32_t)ex;
         if (in) {
-            const bool kept = a || (t && tb < r);
             const uint32_t pos = ab + min(r, tb);
+            const bool kept = (a || (t && tb < r)) && pos < (uint64_t)p.k;  // pos < k: guards a caller's wrong k
             const int64_t I = f / p.nbc, J = f - I * p.nbc;
             p.slot[f] = kept ? (int32_t)pos : -1;
             if (kept) p.colidx[pos] = (int32_t)J;
@@ -641,6 +641,57 @@ __global__ void __launch_bounds__(kThreads, 1) prune_small_kernel(PruneParams p)
     PTRACE(5);
 }
 
+// Pack with a threshold chosen elsewhere (cross-rank global top-k, select_global.cu):
+// keep keys (>> shift) > T and the first `r` keys == T in flat order.  The block
+// sums of squares are already in the workspace (bsr_select_hist level 0).
+template <int ES, int B>
+__global__ void __launch_bounds__(kThreads, 2) prune_apply_kernel(PruneParams p, uint32_t T, int shift, uint32_t r) {
+    using G_ = Geo<ES, B>;
+    __shared__ uint64_t s_warp[32];
+    __shared__ uint32_t s_sel[4];
+    const int64_t u0 = (int64_t)blockIdx.x * p.units / gridDim.x;
+    const int64_t u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
+    auto flat_start = [&](int64_t u) -> int64_t {
+        return u >= p.units ? p.N : (u / p.upr) * p.nbc + (u % p.upr) * G_::G;
+    };
+    const int64_t f0 = flat_start(u0), f1 = flat_start(u1);
+    uint32_t na = 0, nt = 0;
+    for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
+        const uint32_t kk = key_of(p.sumsq[f]) >> shift;
+        na += kk > T;
+        nt += kk == T;
+    }
+    {
+        uint64_t tot;
+        block_excl_scan(((uint64_t)na << 32) | nt, s_warp, tot);
+        if (threadIdx.x == 0) {
+            p.cta_cnt[2 * blockIdx.x] = (uint32_t)(tot >> 32);
+            p.cta_cnt[2 * blockIdx.x + 1] = (uint32_t)tot;
+        }
+    }
+    grid_barrier(p.bar, 0);
+    uint64_t pre = 0;
+    for (int c = threadIdx.x; c < (int)blockIdx.x; c += kThreads)
+        pre += ((uint64_t)__ldcg(p.cta_cnt + 2 * c) << 32) | __ldcg(p.cta_cnt + 2 * c + 1);
+    {
+        uint64_t tot;
+        block_excl_scan(pre, s_warp, tot);
+        pre = tot;
+    }
+    if (threadIdx.x == 0) {  // self-cleaning barrier counter (see prune_kernel)
+        __threadfence();
+        s_sel[3] = atomicAdd(p.bar + 32, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_sel[3] && threadIdx.x == 0) {
+        __threadfence();
+        p.bar[0] = 0;
+        p.bar[32] = 0;
+    }
+    scan_and_index(p, f0, f1, pre, T, shift, r, s_warp);
+    pack_kept<ES, B>(p, u0, u1);
+}
+
 // k == N: every block kept, no norms needed -- a single copy pass.
 template <int ES, int B>
 __global__ void __launch_bounds__(256) keep_all_kernel(PruneParams p) {
@@ -885,6 +936,48 @@ cudaError_t launch_decompress(const int32_t *rowptr, const int32_t *colidx, cons
                                                                          units, upr, Xout);    \
         count_launch();                                                                        \
         return cudaGetLastError();                                                             \
+    }())
+    if (es == 4) {
+        BSRP_DISPATCH_B(4, b, CALL)
+    } else {
+        BSRP_DISPATCH_B(2, b, CALL)
+    }
+#undef CALL
+}
+
+cudaError_t launch_prune_threshold(const void *X, int64_t M, int64_t K, int b, int es, uint32_t T, int shift,
+                                   uint32_t tie_take, int64_t k, int32_t *rowptr, int32_t *colidx, void *values,
+                                   void *ws, cudaStream_t stream) {
+    PruneParams p{};
+    p.X = X;
+    p.K = K;
+    p.nbr = M / b;
+    p.nbc = K / b;
+    p.N = p.nbr * p.nbc;
+    p.k = k;
+    p.rowptr = rowptr;
+    p.colidx = colidx;
+    p.values = values;
+    if (k == 0) return cudaMemsetAsync(rowptr, 0, (size_t)(p.nbr + 1) * 4, stream);
+    const PruneWs w = prune_ws_layout(p.N);
+    char *base = static_cast<char *>(ws);
+    p.bar = reinterpret_cast<uint32_t *>(base + w.hdr);
+    p.cta_cnt = reinterpret_cast<uint32_t *>(base + w.cta_cnt);
+    p.sumsq = reinterpret_cast<float *>(base + w.sumsq);
+    p.slot = reinterpret_cast<int32_t *>(base + w.slot);
+#define CALL(ES_, B_) ([&]() -> cudaError_t {                                                                    \
+        p.upr = units_per_row<ES_, B_>(p.nbc);                                                                  \
+        p.units = p.nbr * p.upr;                                                                                \
+        int occ = 0;                                                                                            \
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, prune_apply_kernel<ES_, B_>, kThreads, 0); \
+        if (e != cudaSuccess) return e;                                                                         \
+        if (occ < 1) return cudaErrorLaunchOutOfResources;                                                      \
+        int64_t grid = std::min<int64_t>((int64_t)occ * num_sms(), kMaxGrid);                                   \
+        grid = std::min<int64_t>(grid, std::max<int64_t>(1, (p.units + kThreads / 32 - 1) / (kThreads / 32)));   \
+        void *args[] = {&p, &T, &shift, &tie_take};                                                             \
+        count_launch();                                                                                         \
+        return cudaLaunchCooperativeKernel((const void *)prune_apply_kernel<ES_, B_>, dim3((unsigned)grid),      \
+                                           dim3(kThreads), args, 0, stream);                                    \
     }())
     if (es == 4) {
         BSRP_DISPATCH_B(4, b, CALL)
