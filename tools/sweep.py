@@ -183,9 +183,36 @@ def sweep_c5(out, hbm, reps=4):
     return rows
 
 
+def sweep_global(out, hbm, reps=20):
+    """f4 at one rank: prune_global (digit-histogram protocol with host round trips,
+    the collectives being no-ops) vs bsr_prune on the same X -- the protocol's
+    fixed cost, and a check that both select the same blocks."""
+    rows = []
+    for lname, M, K, fam in (("fc1", 25088, 384, "aff"), ("fc2", 25088, 1536, "gelu")):
+        X = activation(M, K, fam, SEED + 900, torch.float32)
+        for b in (16, 32):
+            for keep in (0.1, 0.5):
+                A = bp.prune(X, b, keep=keep)
+                t_p = timed(lambda j: bp.prune(X, b, keep=keep, out=A), [0], reps)
+                G = bp.prune_global(X, b, keep)
+                same = bool(torch.equal(G.colidx, A.colidx) and torch.equal(G.rowptr, A.rowptr))
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                for _ in range(reps):
+                    bp.prune_global(X, b, keep)
+                torch.cuda.synchronize()
+                t_g = (time.perf_counter() - t0) / reps * 1e3
+                row = dict(config="f4-global-1rank", layer=lname, M=M, K=K, b=b, keep=keep, prune_ms=t_p,
+                           prune_global_ms_wall=t_g, same_selection=same)
+                rows.append(row)
+                print(json.dumps(row), flush=True)
+                out.write(json.dumps(row) + "\n")
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", nargs="+", choices=["c3", "c5"])
+    ap.add_argument("which", nargs="+", choices=["c3", "c5", "global"])
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out", "sweep"))
     a = ap.parse_args()
     os.makedirs(a.out_dir, exist_ok=True)
@@ -195,7 +222,12 @@ def main():
     for w in a.which:
         with open(os.path.join(a.out_dir, f"{w}.jsonl"), "w") as out:
             out.write(json.dumps(dict(meta=meta)) + "\n")
-            (sweep_c3 if w == "c3" else sweep_c5)(out, hbm, bf16_tf) if w == "c3" else sweep_c5(out, hbm)
+            if w == "c3":
+                sweep_c3(out, hbm, bf16_tf)
+            elif w == "c5":
+                sweep_c5(out, hbm)
+            else:
+                sweep_global(out, hbm)
 
 
 if __name__ == "__main__":
