@@ -24,6 +24,10 @@ other than itself:
   decompress                  equals X * kron(mask, ones) (numpy).
   wgrad / wgrad_entries       keep=1 -> numpy X^T @ dY; any keep ->
                               (X*mask)^T @ dY (numpy matmul); linearity.
+  prune_per_sample            SPEC's per-sample examples (golden
+                              fixture), brute force per sample, count
+                              exactness per sample, numpy segment norms.
+  wgrad_rect                  (X*mask)^T @ dY (numpy matmul) for 1 x b.
 """
 from __future__ import annotations
 
@@ -217,6 +221,40 @@ def wgrad_entries(rowptr, colidx, values, M: int, K: int, b: int, dY: np.ndarray
                                      dY.shape[1], _ptr(rows), _ptr(cols), rows.size, _ptr(out)),
            "wgrad_entries")
     return out
+
+
+def wgrad_rect(rowptr, colidx, values, M: int, K: int, br: int, bc: int, dY: np.ndarray) -> np.ndarray:
+    """fp64 dW = X_bsr^T . dY for br x bc blocks (1 x b row segments for the
+    per-sample variant)."""
+    values = np.ascontiguousarray(values)
+    dY = np.ascontiguousarray(dY)
+    Nout = dY.shape[1]
+    assert dY.shape[0] == M
+    dW = np.empty((K, Nout), dtype=np.float64)
+    _check(_load().orc_wgrad(_ptr(np.ascontiguousarray(rowptr, np.int32)),
+                             _ptr(np.ascontiguousarray(colidx, np.int32)), _ptr(values),
+                             _dtype_code(values), M, K, br, bc, _ptr(dY), _dtype_code(dY), Nout,
+                             _ptr(dW)), "wgrad")
+    return dW
+
+
+def prune_per_sample(X: np.ndarray, b: int, k: int, sample_rows: int):
+    """The paper-faithful variant: 1 x b row-segment blocks
+    (Table II geometry) compared only within one sample --
+    "Blocks are only compared locally, not among other activations in the
+    mini-batch", every sample keeping the same number of blocks.
+    Each run of `sample_rows` rows keeps exactly its k largest-norm segments
+    (ties -> lower flat index, BJ); one BSR (br = 1, bc = b) over all rows.
+
+    Returns dict(rowptr, colidx, values, mask)."""
+    X = np.ascontiguousarray(X)
+    M, K = X.shape
+    if M % sample_rows or K % b:
+        raise ValueError("sample_rows must divide M and b must divide K")
+    masks = [select_topk(block_sumsq(X[s0:s0 + sample_rows], 1, b), k) for s0 in range(0, M, sample_rows)]
+    mask = np.concatenate(masks) if masks else np.zeros(0, np.uint8)
+    rowptr, colidx, values = build_bsr(X, mask, 1, b)
+    return dict(rowptr=rowptr, colidx=colidx, values=values, mask=mask)
 
 
 # ---------------------------------------------------------------- pins / grading

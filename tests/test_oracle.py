@@ -3,6 +3,7 @@
 No GPU.  Each test names the passage or mathematical fact it pins.
 """
 import itertools
+import os
 
 import numpy as np
 import pytest
@@ -321,3 +322,59 @@ def test_brute_force_itself_on_hand_case():
     """Brute force on a hand case: {5,1,1,4} keep 3 -> {0,1,3} (tie -> index 1)."""
     assert list(np.nonzero(oracle.brute_force_topk([25, 1, 1, 16], 3))[0]) == [0, 1, 3]
     assert list(itertools.compress(range(4), oracle.brute_force_topk([25, 1, 1, 16], 2))) == [0, 3]
+
+
+# ---------------------------------------------------------------- f2: 1 x b, per-sample scope
+def _golden_per_sample():
+    rows = {}
+    with open(os.path.join(os.path.dirname(__file__), "golden", "spec_per_sample_b3.txt")) as f:
+        for line in f:
+            if line.strip() and not line.startswith("#"):
+                key, *vals = line.split()
+                rows[key] = vals
+    return np.array([float(v) for v in rows["X"]], dtype=np.float32)[None, :], [int(v) for v in rows["kept"]]
+
+
+def test_per_sample_spec_example():
+    """segments 1 and 3 pruned, nnzb = 2."""
+    X, kept = _golden_per_sample()
+    ref = oracle.prune_per_sample(X, 3, oracle.keep_count(4, 0.5), 1)
+    assert list(np.nonzero(ref["mask"])[0]) == kept
+    assert list(ref["rowptr"]) == [0, 2] and list(ref["colidx"]) == kept
+    np.testing.assert_allclose(oracle.block_norms(X, 1, 3), [3.7417, 0.1732, 4.0, 1.7321], atol=1e-4)
+
+
+def test_per_sample_no_cross_sample_starvation():
+    """sample 0 all large, sample 1 all tiny, keep 0.5 -> each keeps half."""
+    S, K, b = 4, 12, 3
+    X = np.concatenate([np.full((S, K), 10.0, np.float32), np.full((S, K), 1e-3, np.float32)])
+    X += np.arange(2 * S * K, dtype=np.float32).reshape(2 * S, K) * 1e-6  # distinct norms
+    k = oracle.keep_count(S * K // b, 0.5)
+    ref = oracle.prune_per_sample(X, b, k, S)
+    per = ref["mask"].reshape(2, -1).sum(axis=1)
+    assert list(per) == [k, k]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_per_sample_brute_force(seed):
+    rng = np.random.default_rng(seed)
+    S, nsamp, K, b = 3, 3, 8, 2  # 12 segments per sample
+    X = rng.integers(-2, 3, size=(S * nsamp, K)).astype(np.float32)  # exact norms, ties
+    keep = [0.0, 0.25, 0.5, 0.75, 1.0, 0.4][seed]
+    k = oracle.keep_count(S * K // b, keep)
+    ref = oracle.prune_per_sample(X, b, k, S)
+    for s in range(nsamp):
+        seg = (X[s * S:(s + 1) * S].reshape(S, K // b, b) ** 2).sum(-1).reshape(-1).astype(np.float64)
+        want = oracle.brute_force_topk(seg, k)
+        np.testing.assert_array_equal(ref["mask"].reshape(nsamp, -1)[s], want)
+
+
+def test_wgrad_rect_equals_masked_matmul():
+    rng = np.random.default_rng(3)
+    S, nsamp, K, b, N = 5, 4, 24, 4, 7
+    X = rng.standard_normal((S * nsamp, K)).astype(np.float32)
+    dY = rng.standard_normal((S * nsamp, N)).astype(np.float32)
+    ref = oracle.prune_per_sample(X, b, 9, S)
+    dW = oracle.wgrad_rect(ref["rowptr"], ref["colidx"], ref["values"], S * nsamp, K, 1, b, dY)
+    Xm = X.astype(np.float64) * np.repeat(ref["mask"].reshape(S * nsamp, K // b), b, axis=1)
+    np.testing.assert_allclose(dW, Xm.T @ dY.astype(np.float64), rtol=1e-12, atol=1e-12)
