@@ -199,6 +199,35 @@ BSR_API bsr_status_t bsr_prune_threshold(const void *X, int64_t M, int64_t K, in
                                          void *ws, size_t ws_bytes, void *stream);
 
 
+/* ---- the paper-faithful variant: 1 x b row segments, per-sample scope --------
+ * (Table II geometry P:L180-197; "Blocks are only compared
+ * locally, not among other activations in the mini-batch".)
+ * X is M x K with M = samples x sample_rows.  Blocks are 1 x b row segments;
+ * every sample keeps exactly ks = bsr_rows_keep_per_sample(sample_rows, K, b,
+ * keep) = nearest(keep * sample_rows * K / b) segments with the largest fp32 sum
+ * of squares, ties to the lower flat index within the sample.  Output: one BSR
+ * with br = 1, bc = b: rowptr[M + 1], colidx[k] (segment column J, ascending per
+ * row), values[k][b] (raw bits), k = (M / sample_rows) * ks.  Requires b | K,
+ * sample_rows | M and K * sizeof(dtype) % 16 == 0.  The workspace holds the
+ * segment sums (bsr_prune_rows_workspace_bytes).
+ * bsr_decompress_rows: the dense M x K matrix with zeros outside kept segments.
+ * bsr_wgrad_rows: dW (K x N fp32) = X_bsr^T dY over the kept segments, fp32
+ *   FFMA in a fixed order (deterministic); workspace for split partials
+ *   (bsr_wgrad_rows_workspace_bytes, may be 0). */
+BSR_API int64_t bsr_rows_keep_per_sample(int64_t sample_rows, int64_t K, int32_t b, double keep);
+BSR_API size_t bsr_prune_rows_workspace_bytes(int64_t M, int64_t K, int32_t b);
+BSR_API bsr_status_t bsr_prune_rows(const void *X, int64_t M, int64_t K, int32_t b, int64_t sample_rows, double keep,
+                                    int32_t dtype, int32_t *rowptr, int32_t *colidx, void *values, void *ws,
+                                    size_t ws_bytes, void *stream);
+BSR_API bsr_status_t bsr_decompress_rows(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t M,
+                                         int64_t K, int32_t b, int32_t dtype, void *X_out, void *stream);
+BSR_API size_t bsr_wgrad_rows_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N);
+BSR_API bsr_status_t bsr_wgrad_rows(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnz,
+                                    int64_t M, int64_t K, int32_t b, int32_t x_dtype, const void *dY,
+                                    int32_t dy_dtype, int64_t N, float *dW, int32_t accumulate, void *ws,
+                                    size_t ws_bytes, void *stream);
+
+
 /* Static description of a status code. */
 BSR_API const char *bsr_status_string(int32_t status);
 

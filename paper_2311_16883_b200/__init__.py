@@ -20,7 +20,8 @@ from . import _lib
 from ._lib import BsrError, DT_BF16, DT_F32, PREC
 
 __all__ = ["BSR", "BsrError", "prune", "decompress", "wgrad", "block_sumsq", "num_blocks", "keep_count",
-           "storage_bytes", "workspace", "version", "SparseLinear", "sparse_linear", "prune_global"]
+           "storage_bytes", "workspace", "version", "SparseLinear", "sparse_linear", "prune_global",
+           "RowBSR", "prune_rows", "decompress_rows", "wgrad_rows"]
 
 _DT = {torch.float32: DT_F32, torch.bfloat16: DT_BF16}
 
@@ -179,3 +180,4 @@ def wgrad(A: BSR, dY: torch.Tensor, prec: str = "fp32", out: torch.Tensor | None
 
 from .sparse_linear import SparseLinear, sparse_linear  # noqa: E402  (uses the functions above)
 from .global_select import prune_global  # noqa: E402
+from .rows import RowBSR, decompress_rows, prune_rows, wgrad_rows  # noqa: E402

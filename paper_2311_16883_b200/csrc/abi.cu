@@ -238,6 +238,81 @@ bsr_status_t bsr_prune_threshold(const void *X, int64_t M, int64_t K, int32_t b,
     return ok();
 }
 
+/* ---- paper-faithful 1 x b per-sample variant (prune_rows.cu) ---- */
+size_t bsr_prune_rows_workspace_bytes(int64_t M, int64_t K, int32_t b) {
+    if (M <= 0 || K <= 0 || !supported_b(b) || K % b) return 0;
+    return ((size_t)M * (K / b) * 4 + 255) & ~(size_t)255;
+}
+
+int64_t bsr_rows_keep_per_sample(int64_t sample_rows, int64_t K, int32_t b, double keep) {
+    if (sample_rows <= 0 || K <= 0 || b <= 0 || K % b) return -1;
+    return bsr_keep_count(sample_rows * (K / b), keep);
+}
+
+static bsr_status_t check_rows(int64_t M, int64_t K, int32_t b, int32_t dtype) {
+    if (elem_size(dtype) == 0) return fail(BSR_ERR_INVALID_ARG, "dtype %d is not BSR_DT_F32 or BSR_DT_BF16", dtype);
+    if (!supported_b(b)) return fail(BSR_ERR_UNSUPPORTED, "block size b=%d not in {4,8,16,32,64}", b);
+    if (M <= 0 || K <= 0 || K % b) return fail(BSR_ERR_SHAPE, "b=%d must divide K=%lld (M=%lld)", b, (long long)K, (long long)M);
+    if ((K * elem_size(dtype)) % 16) return fail(BSR_ERR_ALIGNMENT, "row pitch of X (K=%lld) is not a multiple of 16 bytes", (long long)K);
+    return BSR_OK;
+}
+
+bsr_status_t bsr_prune_rows(const void *X, int64_t M, int64_t K, int32_t b, int64_t sample_rows, double keep,
+                            int32_t dtype, int32_t *rowptr, int32_t *colidx, void *values, void *ws, size_t ws_bytes,
+                            void *stream) {
+    bsr_status_t st = check_rows(M, K, b, dtype);
+    if (st != BSR_OK) return st;
+    if (!(keep >= 0.0 && keep <= 1.0)) return fail(BSR_ERR_INVALID_ARG, "keep=%g must be in [0, 1]", keep);
+    if (sample_rows <= 0 || M % sample_rows)
+        return fail(BSR_ERR_SHAPE, "sample_rows=%lld must divide M=%lld", (long long)sample_rows, (long long)M);
+    const int64_t ks = bsr_rows_keep_per_sample(sample_rows, K, b, keep);
+    if (!X || !rowptr) return fail(BSR_ERR_INVALID_ARG, "X or rowptr is NULL");
+    if (ks > 0 && (!colidx || !values)) return fail(BSR_ERR_INVALID_ARG, "colidx / values are NULL with k > 0");
+    if (!aligned16(X) || (ks > 0 && !aligned16(values))) return fail(BSR_ERR_ALIGNMENT, "X or values is not 16-byte aligned");
+    const size_t need = bsr_prune_rows_workspace_bytes(M, K, b);
+    if (!ws || ws_bytes < need)
+        return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+    return cuda_status(bsrp::launch_prune_rows(X, M, K, b, elem_size(dtype), sample_rows, ks, rowptr, colidx, values,
+                                               ws, static_cast<cudaStream_t>(stream)),
+                       "bsr_prune_rows launch");
+}
+
+bsr_status_t bsr_decompress_rows(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t M,
+                                 int64_t K, int32_t b, int32_t dtype, void *X_out, void *stream) {
+    bsr_status_t st = check_rows(M, K, b, dtype);
+    if (st != BSR_OK) return st;
+    if (!rowptr || !X_out) return fail(BSR_ERR_INVALID_ARG, "rowptr or X_out is NULL");
+    if (!aligned16(X_out)) return fail(BSR_ERR_ALIGNMENT, "X_out is not 16-byte aligned");
+    return cuda_status(bsrp::launch_decompress_rows(rowptr, colidx, values, M, K, b, elem_size(dtype), X_out,
+                                                    static_cast<cudaStream_t>(stream)),
+                       "bsr_decompress_rows launch");
+}
+
+size_t bsr_wgrad_rows_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N) {
+    if (M <= 0 || K <= 0 || N <= 0 || !supported_b(b) || K % b) return 0;
+    return bsrp::wgrad_rows_ws_bytes(M, K, N);
+}
+
+bsr_status_t bsr_wgrad_rows(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnz, int64_t M,
+                            int64_t K, int32_t b, int32_t x_dtype, const void *dY, int32_t dy_dtype, int64_t N,
+                            float *dW, int32_t accumulate, void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_rows(M, K, b, x_dtype);
+    if (st != BSR_OK) return st;
+    const int esy = elem_size(dy_dtype);
+    if (esy == 0) return fail(BSR_ERR_INVALID_ARG, "dy_dtype %d is not BSR_DT_F32 or BSR_DT_BF16", dy_dtype);
+    if (N <= 0 || (N * esy) % 16 || (N * 4) % 16)
+        return fail(BSR_ERR_ALIGNMENT, "row pitch of dY/dW (N=%lld) is not a multiple of 16 bytes", (long long)N);
+    if (!rowptr || !dY || !dW) return fail(BSR_ERR_INVALID_ARG, "rowptr, dY or dW is NULL");
+    if (nnz > 0 && (!colidx || !values)) return fail(BSR_ERR_INVALID_ARG, "colidx / values are NULL with nnz > 0");
+    if (accumulate != 0 && accumulate != 1) return fail(BSR_ERR_INVALID_ARG, "accumulate must be 0 or 1");
+    const size_t need = bsrp::wgrad_rows_ws_bytes(M, K, N);
+    if (need && (!ws || ws_bytes < need))
+        return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+    return cuda_status(bsrp::launch_wgrad_rows(rowptr, colidx, nnz > 0 ? values : nullptr, elem_size(x_dtype), M, K, b,
+                                               dY, esy, N, dW, accumulate, ws, static_cast<cudaStream_t>(stream)),
+                       "bsr_wgrad_rows launch");
+}
+
 bsr_status_t bsr_decompress(const bsr_t *A, void *X_out, void *stream) {
     bsr_status_t st = check_bsr(A);
     if (st != BSR_OK) return st;

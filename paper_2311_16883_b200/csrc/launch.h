@@ -34,6 +34,16 @@ cudaError_t launch_prune_threshold(const void *X, int64_t M, int64_t K, int b, i
                                    uint32_t tie_take, int64_t k, int32_t *rowptr, int32_t *colidx, void *values,
                                    void *ws, cudaStream_t stream);
 
+// Paper-faithful 1 x b per-sample variant (prune_rows.cu).
+cudaError_t launch_prune_rows(const void *X, int64_t M, int64_t K, int b, int es, int64_t S, int64_t ks,
+                              int32_t *rowptr, int32_t *colidx, void *values, void *ws, cudaStream_t stream);
+cudaError_t launch_decompress_rows(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t M,
+                                   int64_t K, int b, int es, void *out, cudaStream_t stream);
+size_t wgrad_rows_ws_bytes(int64_t M, int64_t K, int64_t N);
+cudaError_t launch_wgrad_rows(const int32_t *rowptr, const int32_t *colidx, const void *values, int es_x, int64_t M,
+                              int64_t K, int b, const void *dY, int es_y, int64_t N, float *dW, int accumulate,
+                              void *ws, cudaStream_t stream);
+
 // dW = X_bsr^T dY, fp32 SIMT path (deterministic); split-K partials in ws.
 size_t wgrad_simt_ws_bytes(int64_t M, int64_t K, int b, int64_t N);
 cudaError_t launch_wgrad_simt(const int32_t *rowptr, const int32_t *colidx, const void *values,
