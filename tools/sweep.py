@@ -210,9 +210,44 @@ def sweep_global(out, hbm, reps=20):
     return rows
 
 
+def sweep_rows(out, hbm, reps=6, nsets=3):
+    """f2: the paper-faithful 1 x b per-sample variant on the S12 layers at batch 128
+    (196-row samples): prune_rows / wgrad_rows / decompress_rows device time."""
+    rows = []
+    S = 196
+    for lname, M, K, N, fam in (("fc1", 25088, 384, 1536, "aff"), ("fc2", 25088, 1536, 384, "gelu")):
+        Xs = [activation(M, K, fam, SEED + 20 * i + 7, torch.float32) for i in range(nsets)]
+        dYs = [grad_out(M, N, SEED + 20 * i + 9, torch.float32) for i in range(nsets)]
+        for b in (4, 8, 16, 32, 64):
+            for keep in (0.1, 0.5, 0.9):
+                As = [bp.prune_rows(X, b, keep, sample_rows=S) for X in Xs]
+                k = As[0].nnz
+                t_p = timed(lambda j: bp.prune_rows(Xs[j], b, keep, sample_rows=S), Xs, reps)
+                dW = torch.empty(K, N, device="cuda")
+                t_w = timed(lambda j: bp.wgrad_rows(As[j], dYs[j], out=dW), Xs, reps)
+                D = torch.empty(M, K, device="cuda")
+                t_d = timed(lambda j: bp.decompress_rows(As[j], out=D), Xs, reps)
+                ref = bp.decompress_rows(As[0]).double().T @ dYs[0].double()
+                err = ((bp.wgrad_rows(As[0], dYs[0]).double() - ref).norm() / ref.norm()).item()
+                bsr = k * b * 4 + 4 * k + 4 * (M + 1)
+                pb = 4 * M * K + bsr
+                row = dict(config="f2-rows", layer=lname, M=M, K=K, N=N, b=b, keep=keep, k=k, sample_rows=S,
+                           prune_ms=t_p, prune_gbs=pb / (t_p * 1e-3) / 1e9, prune_hbm_frac=pb / (t_p * 1e-3) / 1e9 / hbm,
+                           wgrad_ms=t_w, wgrad_tflops=2 * k * b * N / (t_w * 1e-3) / 1e12,
+                           decompress_ms=t_d, decompress_gbs=(bsr + 4 * M * K) / (t_d * 1e-3) / 1e9,
+                           act_bytes_saved=4 * M * K - bsr, check_rel_err=err)
+                rows.append(row)
+                print(json.dumps(row), flush=True)
+                out.write(json.dumps(row) + "\n")
+                del As
+        del Xs, dYs
+        torch.cuda.empty_cache()
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", nargs="+", choices=["c3", "c5", "global"])
+    ap.add_argument("which", nargs="+", choices=["c3", "c5", "global", "rows"])
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out", "sweep"))
     a = ap.parse_args()
     os.makedirs(a.out_dir, exist_ok=True)
@@ -226,8 +261,10 @@ def main():
                 sweep_c3(out, hbm, bf16_tf)
             elif w == "c5":
                 sweep_c5(out, hbm)
-            else:
+            elif w == "global":
                 sweep_global(out, hbm)
+            else:
+                sweep_rows(out, hbm)
 
 
 if __name__ == "__main__":
