@@ -228,6 +228,20 @@ BSR_API bsr_status_t bsr_wgrad_rows(const int32_t *rowptr, const int32_t *colidx
                                     size_t ws_bytes, void *stream);
 
 
+/* ---- producer fusion (the norm pass in the producer of X) -----
+ * bsr_act_block_sumsq: X_out = act(Z) (act 0 = identity, 1 = GELU tanh form,
+ *   evaluated in fp32, rounded to `dtype`), written once, and the fp32 block sums
+ *   of squares of the WRITTEN X (same order and tree as bsr_prune's, so bit-
+ *   identical) into the prune workspace.  Z == X_out (in place) is allowed.
+ * bsr_prune_presummed: bsr_prune_k that takes the block sums from the workspace
+ *   (left there by bsr_act_block_sumsq on the same X, b and workspace) instead of
+ *   reading X for them: X is read only for the kept blocks.  Same output. */
+BSR_API bsr_status_t bsr_act_block_sumsq(const void *Z, void *X_out, int64_t M, int64_t K, int32_t b, int32_t dtype,
+                                         int32_t act, void *ws, size_t ws_bytes, void *stream);
+BSR_API bsr_status_t bsr_prune_presummed(const void *X, int64_t M, int64_t K, int32_t b, int64_t k, int32_t dtype,
+                                         bsr_t *out, void *ws, size_t ws_bytes, void *stream);
+
+
 /* Static description of a status code. */
 BSR_API const char *bsr_status_string(int32_t status);
 

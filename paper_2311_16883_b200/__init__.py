@@ -21,7 +21,7 @@ from ._lib import BsrError, DT_BF16, DT_F32, PREC
 
 __all__ = ["BSR", "BsrError", "prune", "decompress", "wgrad", "block_sumsq", "num_blocks", "keep_count",
            "storage_bytes", "workspace", "version", "SparseLinear", "sparse_linear", "prune_global",
-           "RowBSR", "prune_rows", "decompress_rows", "wgrad_rows"]
+           "RowBSR", "prune_rows", "decompress_rows", "wgrad_rows", "act_prune"]
 
 _DT = {torch.float32: DT_F32, torch.bfloat16: DT_BF16}
 
@@ -138,6 +138,34 @@ def prune(X: torch.Tensor, b: int, keep: float | None = None, k: int | None = No
     _lib.check(lib.bsr_prune_k(X.data_ptr(), M, K, b, k, _dt(X), ctypes.byref(cs), ws.data_ptr(), ws.numel(),
                                _stream(stream)))
     return out
+
+
+def act_prune(Z: torch.Tensor, b: int, keep: float | None = None, k: int | None = None, act: str = "gelu",
+              X_out: torch.Tensor | None = None, out: BSR | None = None, stream=None) -> tuple[torch.Tensor, BSR]:
+    """Producer fusion: X = act(Z) with the block norms computed in
+    the same pass, then the prune reads X only for the kept blocks.  Returns
+    (X, BSR); identical to X = act(Z); prune(X, b, ...)."""
+    lib = _lib.load()
+    Z = _cuda2d(Z, "Z")
+    M, K = Z.shape
+    N = num_blocks(M, K, b)
+    if k is None:
+        if keep is None:
+            raise ValueError("give keep or k")
+        k = keep_count(N, keep)
+    if X_out is None:
+        X_out = torch.empty_like(Z)
+    if out is None:
+        out = alloc_bsr(M, K, b, k, Z.dtype, Z.device)
+    ws_bytes = lib.bsr_prune_workspace_bytes(M, K, b)
+    ws = workspace(ws_bytes, Z.device, kind="prune")
+    a = {"identity": 0, "gelu": 1}[act]
+    _lib.check(lib.bsr_act_block_sumsq(Z.data_ptr(), X_out.data_ptr(), M, K, b, _dt(Z), a, ws.data_ptr(), ws.numel(),
+                                       _stream(stream)))
+    cs = out.c_struct()
+    _lib.check(lib.bsr_prune_presummed(X_out.data_ptr(), M, K, b, k, _dt(Z), ctypes.byref(cs), ws.data_ptr(),
+                                       ws.numel(), _stream(stream)))
+    return X_out, out
 
 
 def block_sumsq(X: torch.Tensor, b: int, stream=None) -> torch.Tensor:

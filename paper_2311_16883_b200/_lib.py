@@ -21,7 +21,7 @@ PREC = {"fp32": 0, "tf32": 1, "bf16": 2}
 EXPORTED = ["bsr_num_blocks", "bsr_keep_count", "bsr_storage_bytes", "bsr_prune_workspace_bytes",
             "bsr_wgrad_workspace_bytes", "bsr_prune", "bsr_prune_k", "bsr_block_sumsq", "bsr_decompress",
             "bsr_wgrad", "bsr_select_hist", "bsr_select_counts", "bsr_prune_threshold", "bsr_rows_keep_per_sample", "bsr_prune_rows_workspace_bytes", "bsr_prune_rows",
-            "bsr_decompress_rows", "bsr_wgrad_rows_workspace_bytes", "bsr_wgrad_rows", "bsr_status_string", "bsr_last_error", "bsr_kernel_launches", "bsr_version"]
+            "bsr_decompress_rows", "bsr_wgrad_rows_workspace_bytes", "bsr_wgrad_rows", "bsr_act_block_sumsq", "bsr_prune_presummed", "bsr_status_string", "bsr_last_error", "bsr_kernel_launches", "bsr_version"]
 
 
 class BsrT(ctypes.Structure):
@@ -71,6 +71,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "bsr_decompress_rows": (i32, [vp, vp, vp, i64, i64, i32, i32, vp, vp]),
         "bsr_wgrad_rows_workspace_bytes": (sz, [i64, i64, i32, i64]),
         "bsr_wgrad_rows": (i32, [vp, vp, vp, i64, i64, i64, i32, i32, vp, i32, i64, vp, i32, vp, sz, vp]),
+        "bsr_act_block_sumsq": (i32, [vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]),
+        "bsr_prune_presummed": (i32, [vp, i64, i64, i32, i64, i32, P, vp, sz, vp]),
         "bsr_status_string": (ctypes.c_char_p, [i32]),
         "bsr_last_error": (ctypes.c_char_p, []),
         "bsr_kernel_launches": (ctypes.c_uint64, []),

@@ -115,7 +115,7 @@ size_t bsr_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int
 }
 
 static bsr_status_t prune_impl(const void *X, int64_t M, int64_t K, int32_t b, int64_t k, int32_t dtype,
-                               bsr_t *out, void *ws, size_t ws_bytes, void *stream) {
+                               bsr_t *out, void *ws, size_t ws_bytes, void *stream, int presummed = 0) {
     bsr_status_t st = check_shape(M, K, b, dtype);
     if (st != BSR_OK) return st;
     const int64_t N = (M / b) * (K / b);
@@ -138,8 +138,9 @@ static bsr_status_t prune_impl(const void *X, int64_t M, int64_t K, int32_t b, i
             return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
         if (!aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
     }
+    if (presummed && !(ws && ws_bytes >= need)) return fail(BSR_ERR_WORKSPACE, "presummed prune needs the workspace");
     cudaError_t e = bsrp::launch_prune(X, M, K, b, es, k, out->rowptr, out->colidx, out->values, ws,
-                                       static_cast<cudaStream_t>(stream));
+                                       static_cast<cudaStream_t>(stream), presummed);
     if (e != cudaSuccess) return cuda_status(e, "bsr_prune launch");
     out->M = M;
     out->K = K;
@@ -311,6 +312,29 @@ bsr_status_t bsr_wgrad_rows(const int32_t *rowptr, const int32_t *colidx, const 
     return cuda_status(bsrp::launch_wgrad_rows(rowptr, colidx, nnz > 0 ? values : nullptr, elem_size(x_dtype), M, K, b,
                                                dY, esy, N, dW, accumulate, ws, static_cast<cudaStream_t>(stream)),
                        "bsr_wgrad_rows launch");
+}
+
+/* ---- producer fusion ---- */
+bsr_status_t bsr_act_block_sumsq(const void *Z, void *X_out, int64_t M, int64_t K, int32_t b, int32_t dtype,
+                                 int32_t act, void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_shape(M, K, b, dtype);
+    if (st != BSR_OK) return st;
+    if (act != 0 && act != 1) return fail(BSR_ERR_INVALID_ARG, "act=%d must be 0 (identity) or 1 (GELU, tanh form)", act);
+    if (!Z || !X_out) return fail(BSR_ERR_INVALID_ARG, "Z or X_out is NULL");
+    if (!aligned16(Z) || !aligned16(X_out)) return fail(BSR_ERR_ALIGNMENT, "Z or X_out is not 16-byte aligned");
+    const size_t xb = (size_t)M * K * elem_size(dtype);
+    if (Z != X_out && overlap(Z, xb, X_out, xb)) return fail(BSR_ERR_INVALID_ARG, "Z and X_out overlap partially");
+    const size_t need = bsrp::prune_ws_layout((M / b) * (K / b)).total;
+    if (!ws || ws_bytes < need)
+        return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+    return cuda_status(bsrp::launch_act_sumsq(Z, X_out, M, K, b, elem_size(dtype), act, ws,
+                                              static_cast<cudaStream_t>(stream)),
+                       "bsr_act_block_sumsq launch");
+}
+
+bsr_status_t bsr_prune_presummed(const void *X, int64_t M, int64_t K, int32_t b, int64_t k, int32_t dtype, bsr_t *out,
+                                 void *ws, size_t ws_bytes, void *stream) {
+    return prune_impl(X, M, K, b, k, dtype, out, ws, ws_bytes, stream, 1);
 }
 
 bsr_status_t bsr_decompress(const bsr_t *A, void *X_out, void *stream) {

@@ -19,7 +19,10 @@ PruneWs prune_ws_layout(int64_t N);
 // Returns cudaSuccess or the launch error.
 cudaError_t launch_prune(const void *X, int64_t M, int64_t K, int b, int es, int64_t k,
                          int32_t *rowptr, int32_t *colidx, void *values, void *ws,
-                         cudaStream_t stream);
+                         cudaStream_t stream, int presummed = 0);
+// Producer fusion: X = act(Z) and the block sums (into the prune workspace) in one pass.
+cudaError_t launch_act_sumsq(const void *Z, void *X, int64_t M, int64_t K, int b, int es, int act, void *ws,
+                             cudaStream_t stream);
 cudaError_t launch_block_sumsq(const void *X, int64_t M, int64_t K, int b, int es, float *sumsq,
                                cudaStream_t stream);
 cudaError_t launch_decompress(const int32_t *rowptr, const int32_t *colidx, const void *values,

@@ -52,6 +52,7 @@ struct PruneParams {
     int32_t *slot;
     uint32_t *bar, *hist1, *hist2, *hist3, *cta_cnt;
     uint2 *cand;  // [kCandMax] (key, flat index) of the boundary bin's blocks
+    int presummed;  // 1: block sums already in `sumsq` (act_sumsq_kernel); phase 1 skips X
 };
 
 // Selection key of a block: fp32 bits of sumsq (>= 0, so the integer order is
@@ -264,13 +265,17 @@ __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
     // ---------------- phase 1: block sums of squares + level-1 histogram
     for (int i = threadIdx.x; i < kH1; i += kThreads) s_hist[i] = 0;
     __syncthreads();
-    for (int64_t u = u0 + wid; u < u1; u += nw) {
-        const int64_t I = u / p.upr, J = (u % p.upr) * G_::G + j;
-        const bool valid = J < p.nbc;
-        float s = block_sumsq_warp<ES, B>(p.X, p.K, I, J, sub, valid);
-        if (valid && sub == 0) {
-            p.sumsq[I * p.nbc + J] = s;
-            atomicAdd(&s_hist[key_of(s) >> 19], 1u);
+    if (p.presummed) {  // sums written by the producer (act_sumsq_kernel): X is not read here
+        for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) atomicAdd(&s_hist[key_of(p.sumsq[f]) >> 19], 1u);
+    } else {
+        for (int64_t u = u0 + wid; u < u1; u += nw) {
+            const int64_t I = u / p.upr, J = (u % p.upr) * G_::G + j;
+            const bool valid = J < p.nbc;
+            float s = block_sumsq_warp<ES, B>(p.X, p.K, I, J, sub, valid);
+            if (valid && sub == 0) {
+                p.sumsq[I * p.nbc + J] = s;
+                atomicAdd(&s_hist[key_of(s) >> 19], 1u);
+            }
         }
     }
     __syncthreads();
@@ -724,6 +729,79 @@ __global__ void __launch_bounds__(256) keep_all_kernel(PruneParams p) {
     }
 }
 
+// Producer fusion: X = act(Z) written once, and the block sums
+// of squares of the written X accumulated in the same pass -- same per-element
+// order and reduction tree as block_sumsq_warp, so the sums are bit-identical to
+// the ones prune_kernel's phase 1 would compute from X.  A later prune with
+// `presummed` skips phase 1's read of X.  act: 0 = identity, 1 = GELU (tanh form).
+__device__ __forceinline__ float act_fn(float z, int act) {
+    if (act == 1) {
+        const float u = 0.7978845608028654f * fmaf(0.044715f * z, z * z, z);
+        return 0.5f * z * (1.0f + tanhf(u));
+    }
+    return z;
+}
+
+template <int ES, int B>
+__global__ void __launch_bounds__(256) act_sumsq_kernel(const void *Z, void *X, int64_t K, int64_t nbc, int64_t units,
+                                                        int64_t upr, int act, float *sumsq) {
+    using G_ = Geo<ES, B>;
+    using V = typename G_::V;
+    const int lane = threadIdx.x & 31;
+    const int j = lane / G_::LPB, sub = lane % G_::LPB;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t u = wg; u < units; u += nwg) {
+        const int64_t I = u / upr, J = (u % upr) * G_::G + j;
+        const bool valid = J < nbc;
+        float acc[G_::EPV];
+#pragma unroll
+        for (int e = 0; e < G_::EPV; ++e) acc[e] = 0.f;
+        if (valid) {
+            const int64_t rs = K / G_::EPV;
+            const V *src = reinterpret_cast<const V *>(Z) + (I * B) * rs + (J * B) / G_::EPV + sub;
+            V *dst = reinterpret_cast<V *>(X) + (I * B) * rs + (J * B) / G_::EPV + sub;
+#pragma unroll
+            for (int r0 = 0; r0 < B; r0 += G_::R) {
+                V v[G_::R];
+#pragma unroll
+                for (int rr = 0; rr < G_::R; ++rr) v[rr] = ld_stream(src + (r0 + rr) * rs);
+#pragma unroll
+                for (int rr = 0; rr < G_::R; ++rr) {
+                    uint32_t w[G_::VB / 4];
+#pragma unroll
+                    for (int q = 0; q < G_::VB / 4; ++q) w[q] = word(v[rr], q);
+#pragma unroll
+                    for (int e = 0; e < G_::EPV; ++e) {
+                        float x = act_fn(elem<ES>(v[rr], e), act);
+                        if constexpr (ES == 4) {
+                            w[e] = __float_as_uint(x);
+                        } else {
+                            const uint32_t h = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x));
+                            x = __uint_as_float(h << 16);
+                            w[e >> 1] = (e & 1) ? ((w[e >> 1] & 0xffffu) | (h << 16)) : ((w[e >> 1] & 0xffff0000u) | h);
+                        }
+                        acc[e] = fmaf(x, x, acc[e]);
+                    }
+                    V o;
+                    if constexpr (G_::VB == 16) o = make_uint4(w[0], w[1], w[2], w[3]);
+                    else if constexpr (G_::VB == 8) o = make_uint2(w[0], w[1]);
+                    else o = w[0];
+                    dst[(r0 + rr) * rs] = o;
+                }
+            }
+        }
+#pragma unroll
+        for (int w = 1; w < G_::EPV; w <<= 1)
+#pragma unroll
+            for (int e = 0; e < G_::EPV; e += 2 * w) acc[e] = acc[e] + acc[e + w];
+        float s = acc[0];
+#pragma unroll
+        for (int off = 1; off < G_::LPB; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (valid && sub == 0) sumsq[I * nbc + J] = s;
+    }
+}
+
 // Test hook: phase 1 only, written to a caller buffer.
 template <int ES, int B>
 __global__ void __launch_bounds__(256) sumsq_kernel(const void *X, int64_t K, int64_t nbc, int64_t units,
@@ -834,7 +912,7 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
     }
     // (no per-launch memset: the kernel leaves its workspace header zeroed, see above)
     cudaError_t e = cudaSuccess;
-    if (p.N <= kSmallN && small_path_enabled()) {
+    if (p.N <= kSmallN && small_path_enabled() && !p.presummed) {
         const size_t smem = (size_t)((p.N + 3) & ~int64_t(3)) * 4 + (size_t)kCandCap * 4;
         e = cudaFuncSetAttribute(prune_small_kernel<ES, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -877,8 +955,9 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
     }
 
 cudaError_t launch_prune(const void *X, int64_t M, int64_t K, int b, int es, int64_t k, int32_t *rowptr,
-                         int32_t *colidx, void *values, void *ws, cudaStream_t stream) {
+                         int32_t *colidx, void *values, void *ws, cudaStream_t stream, int presummed) {
     PruneParams p{};
+    p.presummed = presummed;
     p.X = X;
     p.K = K;
     p.nbr = M / b;
@@ -900,6 +979,25 @@ cudaError_t launch_prune(const void *X, int64_t M, int64_t K, int b, int es, int
     p.cand = reinterpret_cast<uint2 *>(base + w.cand);
 #define CALL(ES_, B_) (p.upr = units_per_row<ES_, B_>(p.nbc), p.units = p.nbr * p.upr, \
                        launch_prune_t<ES_, B_>(p, stream, ws, w))
+    if (es == 4) {
+        BSRP_DISPATCH_B(4, b, CALL)
+    } else {
+        BSRP_DISPATCH_B(2, b, CALL)
+    }
+#undef CALL
+}
+
+cudaError_t launch_act_sumsq(const void *Z, void *X, int64_t M, int64_t K, int b, int es, int act, void *ws,
+                             cudaStream_t stream) {
+    const int64_t nbr = M / b, nbc = K / b;
+    float *sumsq = reinterpret_cast<float *>(static_cast<char *>(ws) + prune_ws_layout(nbr * nbc).sumsq);
+#define CALL(ES_, B_) ([&]() {                                                                        \
+        int64_t upr = units_per_row<ES_, B_>(nbc), units = nbr * upr;                               \
+        int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((units + 7) / 8, 148 * 16));           \
+        act_sumsq_kernel<ES_, B_><<<(unsigned)blocks, 256, 0, stream>>>(Z, X, K, nbc, units, upr, act, sumsq); \
+        count_launch();                                                                             \
+        return cudaGetLastError();                                                                  \
+    }())
     if (es == 4) {
         BSRP_DISPATCH_B(4, b, CALL)
     } else {

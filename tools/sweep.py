@@ -245,9 +245,41 @@ def sweep_rows(out, hbm, reps=6, nsets=3):
     return rows
 
 
+def sweep_fusion(out, hbm, reps=20, nsets=3):
+    """f3 (norm in the producer): GELU(Z) + bsr_prune vs the fused
+    bsr_act_block_sumsq + bsr_prune_presummed, S12 fc2 input (25088 x 1536) and
+    the C2 shape (25088 x 384), b 16/32, keep 0.1/0.5."""
+    rows = []
+    for lname, M, K in (("fc2-input", 25088, 1536), ("fc1-input", 25088, 384)):
+        Zs = [activation(M, K, "aff", SEED + 40 + i, torch.float32) for i in range(nsets)]
+        Xs = [torch.empty_like(Z) for Z in Zs]
+        for b in (16, 32):
+            for keep in (0.1, 0.5):
+                k = bp.keep_count(bp.num_blocks(M, K, b), keep)
+                As = [bp.alloc_bsr(M, K, b, k, torch.float32, "cuda") for _ in range(nsets)]
+
+                def unfused(j):  # PyTorch's GELU kernel (one read of Z, one write of X), then the prune
+                    bp.prune(torch.nn.functional.gelu(Zs[j], approximate="tanh"), b, k=k, out=As[j])
+
+                def gelu_only(j):
+                    torch.nn.functional.gelu(Zs[j], approximate="tanh")
+
+                t_u = timed(unfused, Zs, reps)
+                t_g = timed(gelu_only, Zs, reps)
+                t_f = timed(lambda j: bp.act_prune(Zs[j], b, k=k, act="gelu", X_out=Xs[j], out=As[j]), Zs, reps)
+                row = dict(config="f3-fusion", layer=lname, M=M, K=K, b=b, keep=keep,
+                           unfused_ms=t_u, torch_gelu_ms=t_g, fused_ms=t_f, saved_ms=t_u - t_f)
+                rows.append(row)
+                print(json.dumps(row), flush=True)
+                out.write(json.dumps(row) + "\n")
+        del Zs, Xs
+        torch.cuda.empty_cache()
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", nargs="+", choices=["c3", "c5", "global", "rows"])
+    ap.add_argument("which", nargs="+", choices=["c3", "c5", "global", "rows", "fusion"])
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out", "sweep"))
     a = ap.parse_args()
     os.makedirs(a.out_dir, exist_ok=True)
@@ -263,8 +295,10 @@ def main():
                 sweep_c5(out, hbm)
             elif w == "global":
                 sweep_global(out, hbm)
-            else:
+            elif w == "rows":
                 sweep_rows(out, hbm)
+            else:
+                sweep_fusion(out, hbm)
 
 
 if __name__ == "__main__":
