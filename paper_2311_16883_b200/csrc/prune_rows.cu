@@ -99,18 +99,36 @@ __device__ __forceinline__ uint64_t scan64(uint64_t v, uint64_t *s_warp, uint64_
     return base + x - v;
 }
 
+constexpr int kSmemKeys = 12288;  // a sample's keys staged in shared memory when they fit (48 KB)
+
 template <int ES, int B>
 __global__ void __launch_bounds__(kThreads) rows_select_kernel(const uint8_t *__restrict__ X, int64_t K, int64_t S,
-                                                               int64_t ks, const float *__restrict__ sumsq,
+                                                               int64_t ks, const float *__restrict__ sumsq_g,
                                                                int32_t *__restrict__ rowptr,
                                                                int32_t *__restrict__ colidx,
                                                                uint8_t *__restrict__ values) {
     __shared__ uint32_t s_h[256];
     __shared__ uint64_t s_warp[32];
     __shared__ uint32_t s_sel[3];
+    extern __shared__ float s_keys[];
     const int lane = threadIdx.x & 31;
     const int64_t nbc = K / B, ns = S * nbc;
     const int64_t s = blockIdx.x, f0 = s * ns;
+    // the passes below re-read the sample's keys several times: from shared memory
+    // when they fit (several independent loads in flight while staging them)
+    const bool on_chip = ns <= kSmemKeys;
+    if (on_chip) {
+        for (int64_t i0 = threadIdx.x; i0 < ns; i0 += 4 * kThreads) {
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = i0 + u * kThreads < ns ? __ldcg(sumsq_g + f0 + i0 + u * kThreads) : 0.f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i0 + u * kThreads < ns) s_keys[i0 + u * kThreads] = v[u];
+        }
+        __syncthreads();
+    }
+    auto keyat = [&](int64_t f) -> float { return on_chip ? s_keys[f] : __ldcg(sumsq_g + f0 + f); };
     const int64_t out0 = s * ks;  // this sample's first output slot
     if (s == 0 && threadIdx.x == 0) rowptr[0] = 0;
     uint32_t prefix = 0, need = (uint32_t)ks;
@@ -122,7 +140,7 @@ __global__ void __launch_bounds__(kThreads) rows_select_kernel(const uint8_t *__
             __syncthreads();
             for (int64_t fb = 0; fb < ns; fb += kThreads) {
                 const int64_t f = fb + threadIdx.x;
-                const uint32_t key = f < ns ? key_of(__ldcg(sumsq + f0 + f)) : 0u;
+                const uint32_t key = f < ns ? key_of(keyat(f)) : 0u;
                 const bool in = f < ns && (pass == 0 || (key >> shift) == prefix);
                 const uint32_t bin = (key >> nshift) & ((1u << w) - 1u);
                 const uint32_t im = __ballot_sync(0xffffffffu, in);
@@ -165,7 +183,7 @@ __global__ void __launch_bounds__(kThreads) rows_select_kernel(const uint8_t *__
         const int64_t f = fb + threadIdx.x;
         uint32_t a = 0, t = 0;
         if (f < ns) {
-            const uint32_t kk = key_of(__ldcg(sumsq + f0 + f)) >> shift;
+            const uint32_t kk = key_of(keyat(f)) >> shift;
             if (ks == ns) {
                 a = 1;
             } else if (ks > 0) {
@@ -253,6 +271,9 @@ __global__ void __launch_bounds__(kWT, 2) rows_wgrad_kernel(WParams p) {
     const int nbc = (int)(p.K / B), J0 = (int)(kc0 / B), nbJ = min(kKT / B, nbc - J0);
     const int64_t ngroups = (p.M + kR - 1) / kR;
     const int64_t Gb = (int64_t)split * ngroups / p.nsplit, Ge = (int64_t)(split + 1) * ngroups / p.nsplit;
+    // this warp's kcols [16w, 16w + 16) of the range -> segment columns (range-relative)
+    const int wj0 = (warp * 16) / B, wj1 = (warp * 16 + 15) / B;
+    const uint32_t wmask = (wj1 >= 31 ? 0xffffffffu : ((1u << (wj1 + 1)) - 1u)) & ~((1u << wj0) - 1u);
 
     float acc[8][8];
 #pragma unroll
@@ -342,6 +363,7 @@ __global__ void __launch_bounds__(kWT, 2) rows_wgrad_kernel(WParams p) {
             const uint8_t *xs = smem + cur * STAGE, *ys = xs + XB;
 #pragma unroll 4
             for (int r = 0; r < kR; ++r) {
+                if (!(s_mask[buf][r] & wmask)) continue;  // this row keeps no segment in the warp's 16 kcols
                 float xv[8], yv[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
@@ -416,7 +438,9 @@ cudaError_t launch_prune_rows(const void *X, int64_t M, int64_t K, int b, int es
 #define CALL(ES_, B_) ([&]() -> cudaError_t {                                                                      \
         rows::rows_sumsq_kernel<ES_, B_><<<g1, 256, 0, stream>>>(static_cast<const uint8_t *>(X), M, K, sumsq);    \
         count_launch();                                                                                           \
-        rows::rows_select_kernel<ES_, B_><<<(unsigned)(M / S), rows::kThreads, 0, stream>>>(                       \
+        const int64_t ns_ = S * (K / B_);                                                                         \
+        const size_t smem_ = ns_ <= rows::kSmemKeys ? (size_t)ns_ * 4 : 0;                                        \
+        rows::rows_select_kernel<ES_, B_><<<(unsigned)(M / S), rows::kThreads, smem_, stream>>>(                   \
             static_cast<const uint8_t *>(X), K, S, ks, sumsq, rowptr, colidx, static_cast<uint8_t *>(values));     \
         count_launch();                                                                                           \
         return cudaGetLastError();                                                                                \
