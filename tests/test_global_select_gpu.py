@@ -67,10 +67,11 @@ def _worker(rank, world, port, X, b, keep, rows, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("family,b,keep", [("ints", 16, 0.37), ("aff", 32, 0.5), ("ints", 4, 0.8)])
-def test_two_ranks_equal_concatenated_oracle(family, b, keep):
-    M, K = 48 * b, 8 * b
-    rows = [(0, 20 * b), (20 * b, M)]  # unequal shards
+@pytest.mark.parametrize("family,b,keep,shape", [("ints", 16, 0.37, None), ("aff", 32, 0.5, None), ("ints", 4, 0.8, None),
+                                                 ("aff", 32, 0.5, (25088, 384))])  # the last: C2 at full size
+def test_two_ranks_equal_concatenated_oracle(family, b, keep, shape):
+    M, K = shape if shape else (48 * b, 8 * b)
+    rows = [(0, (M // b * 5 // 12) * b), ((M // b * 5 // 12) * b, M)]  # unequal shards
     k = oracle.keep_count(oracle.num_blocks(M, K, b), keep)
     X = _x(family, M, K, 5, b, k)
     ctx = mp.get_context("spawn")

@@ -102,3 +102,20 @@ def test_rows_s12_fc1_shape():
     assert all(rp[(s + 1) * S] - rp[s * S] == ks for s in range(nsamp))
     want = oracle.wgrad_rect(rp, A.colidx.cpu().numpy(), A.values.cpu().numpy().reshape(-1, 1, b), M, K, 1, b, dY)
     assert oracle.rel_frobenius(dW.cpu().numpy(), want) <= 1e-5
+
+
+def test_rows_selection_full_s12_batch():
+    """C3 geometry at the full batch (128 samples x 196 tokens x 384 channels,
+    b = 16, keep 0.5): every sample's selection and packed values bit-exact
+    against the oracle (integer-valued X: exact fp32 sums, ties resolved by the
+    BJ rule)."""
+    S, nsamp, K, b = 196, 128, 384, 16
+    M = S * nsamp
+    X = synth.ints(M, K, 21)
+    ks = oracle.keep_count(S * K // b, 0.5)
+    ref = oracle.prune_per_sample(X, b, ks, S)
+    A = bp.prune_rows(to_torch(X), b, 0.5, sample_rows=S)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(A.rowptr.cpu().numpy(), ref["rowptr"])
+    np.testing.assert_array_equal(A.colidx.cpu().numpy(), ref["colidx"])
+    np.testing.assert_array_equal(A.values.cpu().numpy().view(np.int32), ref["values"].reshape(-1, b).view(np.int32))
