@@ -1107,17 +1107,22 @@ size_t wgrad_tc_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
     return std::max(wgrad_runs_ws_bytes(M, K, b, N), wgrad_span_ws_bytes(M, K, b, N));
 }
 
-// Kernel choice: the per-run kernel above unless BSRP_WGRAD=span selects the
-// experimental span kernel (wgrad_span.cu; measured slower at C2).
-static bool use_runs_kernel() {
+// Kernel choice (measured): the per-run kernel, except for b = 16
+// with many block columns (K / b >= 64, e.g. S12 fc2 with bf16), where its one
+// MMA per run of N = 16..64 columns is issue-bound and the span kernel's
+// dense-padded N <= 256 MMAs win (fc2 bf16 keep 0.5: 124 vs 200 us).
+// BSRP_WGRAD=runs|span forces one (measurements, tests).
+static bool use_runs_kernel(int b, int64_t K) {
     const char *e = std::getenv("BSRP_WGRAD");
-    return !(e && std::string(e) == "span");
+    if (e && std::string(e) == "span") return false;
+    if (e && std::string(e) == "runs") return true;
+    return !(b == 16 && K / b >= 64);
 }
 
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
                             int kind, int64_t M, int64_t K, int b, const void *dY, int64_t N, float *dW,
                             int accumulate, void *ws, cudaStream_t stream) {
-    if (!use_runs_kernel())
+    if (!use_runs_kernel(b, K))
         return launch_wgrad_span(rowptr, colidx, values, nnzb, kind, M, K, b, dY, N, dW, accumulate, ws, stream);
     if (!values || nnzb == 0) {  // no stored block: dW = 0 (or unchanged)
         return accumulate ? cudaSuccess : cudaMemsetAsync(dW, 0, (size_t)K * N * sizeof(float), stream);

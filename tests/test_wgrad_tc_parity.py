@@ -26,11 +26,14 @@ import paper_2311_16883_b200 as bp  # noqa: E402
 TOL = 5e-3
 
 
-@pytest.fixture(autouse=True, params=["runs", "span"])
+@pytest.fixture(autouse=True, params=["runs", "span", "auto"])
 def wgrad_kernel(request, monkeypatch):
-    """Every case runs on both tcgen05 dW kernels: the default per-run kernel and the
-    experimental span kernel (CTA-pair MMAs; BSRP_WGRAD=span)."""
-    monkeypatch.setenv("BSRP_WGRAD", request.param)
+    """Every case runs on both tcgen05 dW kernels -- the per-run kernel and the span
+    kernel (CTA-pair MMAs) -- and on the library's own per-shape choice."""
+    if request.param == "auto":
+        monkeypatch.delenv("BSRP_WGRAD", raising=False)
+    else:
+        monkeypatch.setenv("BSRP_WGRAD", request.param)
     return request.param
 
 
