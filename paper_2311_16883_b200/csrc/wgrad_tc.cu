@@ -1107,16 +1107,17 @@ size_t wgrad_tc_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
     return std::max(wgrad_runs_ws_bytes(M, K, b, N), wgrad_span_ws_bytes(M, K, b, N));
 }
 
-// Kernel choice (measured): the per-run kernel, except for b = 16
-// with many block columns (K / b >= 64, e.g. S12 fc2 with bf16), where its one
-// MMA per run of N = 16..64 columns is issue-bound and the span kernel's
-// dense-padded N <= 256 MMAs win (fc2 bf16 keep 0.5: 124 vs 200 us).
-// BSRP_WGRAD=runs|span forces one (measurements, tests).
+// Kernel choice (measured): the per-run kernel, except with many
+// block columns (K / b >= 64: S12 fc2 at b = 16, B24 fc2 at b = 32), where it
+// splits the kcols into several TMEM ranges that each re-read dY and issues one
+// MMA per short run, while the span kernel's CTA pairs and dense-padded
+// N <= 256 MMAs win (S12 fc2 bf16 b=16: 124 vs 200 us; B24 fc2 b=32: 2.38 vs
+// 3.92 ms f32/tf32, 1.45 vs 2.91 ms bf16).  BSRP_WGRAD=runs|span forces one.
 static bool use_runs_kernel(int b, int64_t K) {
     const char *e = std::getenv("BSRP_WGRAD");
     if (e && std::string(e) == "span") return false;
     if (e && std::string(e) == "runs") return true;
-    return !(b == 16 && K / b >= 64);
+    return K / b < 64;
 }
 
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
