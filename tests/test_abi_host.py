@@ -131,3 +131,33 @@ def test_decompress_and_wgrad_validation(lib):
 def test_status_strings(lib):
     for code, name in _lib.STATUS_NAMES.items():
         assert lib.bsr_status_string(code).decode() == name
+
+
+def test_variant_calls_validation(lib):
+    """Argument checks of the §8f variants' entry points (host-side, before any launch)."""
+    WS, BIG = FAKE + 0x800000, 1 << 30
+    H = FAKE + 0x2000000
+    # global selection (f4)
+    assert lib.bsr_select_hist(FAKE, 256, 256, 16, 0, 3, 0, H, WS, BIG, None) == 1          # level
+    assert lib.bsr_select_hist(FAKE, 256, 256, 16, 0, 0, 0, None, WS, BIG, None) == 1       # hist
+    assert lib.bsr_select_hist(FAKE, 256, 256, 5, 0, 0, 0, H, WS, BIG, None) == 3           # b
+    assert lib.bsr_select_hist(FAKE, 256, 256, 16, 0, 0, 0, H, WS, 16, None) == 5           # workspace
+    assert lib.bsr_select_counts(256, 256, 16, 0, 5, H, WS, BIG, None) == 1                 # shift
+    out = _lib.BsrT(0, 0, 0, 0, 0, FAKE + 0x100000, FAKE + 0x200000, FAKE + 0x300000)
+    assert lib.bsr_prune_threshold(FAKE, 256, 256, 16, 0, 0, 0, 11, 10, ctypes.byref(out), WS, BIG, None) == 1
+    assert lib.bsr_prune_threshold(FAKE, 256, 256, 16, 0, 0, 0, 0, 257, ctypes.byref(out), WS, BIG, None) == 1
+    # 1 x b per-sample variant (f2)
+    assert lib.bsr_rows_keep_per_sample(196, 384, 16, 0.5) == 2352
+    assert lib.bsr_rows_keep_per_sample(196, 383, 16, 0.5) == -1
+    assert lib.bsr_prune_rows_workspace_bytes(392, 384, 16) == 392 * 24 * 4
+    assert lib.bsr_prune_rows(FAKE, 392, 384, 16, 100, 0.5, 0, FAKE, FAKE, FAKE, WS, BIG, None) == 2  # sample_rows
+    assert lib.bsr_prune_rows(FAKE, 392, 384, 16, 196, 1.5, 0, FAKE, FAKE, FAKE, WS, BIG, None) == 1  # keep
+    assert lib.bsr_prune_rows(FAKE, 392, 12, 4, 196, 0.5, 1, FAKE, FAKE, FAKE, WS, BIG, None) == 4    # bf16 pitch 24 B
+    assert lib.bsr_prune_rows(FAKE, 392, 384, 16, 196, 0.5, 0, FAKE, FAKE, FAKE, WS, 8, None) == 5    # workspace
+    assert lib.bsr_wgrad_rows(FAKE, FAKE, FAKE, 10, 392, 384, 16, 0, FAKE, 0, 6, FAKE, 0, None, 0, None) == 4  # N pitch
+    assert lib.bsr_wgrad_rows(FAKE, FAKE, FAKE, 10, 392, 384, 16, 0, FAKE, 0, 256, FAKE, 2, None, 0, None) == 1
+    # producer fusion (f3)
+    assert lib.bsr_act_block_sumsq(FAKE, FAKE, 256, 256, 16, 0, 2, WS, BIG, None) == 1       # act
+    assert lib.bsr_act_block_sumsq(FAKE, FAKE + 8, 256, 256, 16, 0, 1, WS, BIG, None) == 4   # alignment
+    assert lib.bsr_act_block_sumsq(FAKE, FAKE, 256, 256, 16, 0, 1, WS, 8, None) == 5         # workspace
+    assert lib.bsr_prune_presummed(FAKE, 256, 256, 16, 10, 0, ctypes.byref(out), None, 0, None) == 5
