@@ -299,102 +299,105 @@ __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
         // bin and appends its keys inside the bin, with their flat index, to a
         // global list.  After the barrier each CTA resolves the exact threshold
         // from the list and its own prefix counts (CTAs before it + listed keys
-        // before its range), unless the bin overflowed the list.
-        const uint32_t prefix1 = prefix;
-        // pass A: this CTA's counts (keys above the bin, keys in it) -> one atomic
-        // reservation of list slots per CTA (a single hot counter would serialise)
-        uint32_t na = 0, ni = 0;
-        for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
-            const uint32_t hb = key_of(p.sumsq[f]) >> 19;
-            na += hb > prefix1;
-            ni += hb == prefix1;
-        }
-        uint32_t slot0, ni_cta;
-        {
-            uint64_t tot;
-            block_excl_scan(((uint64_t)na << 32) | ni, s_warp, tot);
-            ni_cta = (uint32_t)tot;
-            if (threadIdx.x == 0) {
-                p.cta_cnt[2 * blockIdx.x] = (uint32_t)(tot >> 32);
-                s_sel[3] = (uint32_t)tot ? atomicAdd(p.bar + 16, (uint32_t)tot) : 0u;
+        // before its range) -- when the bin fits the list.
+        if (bincnt <= (uint32_t)kCandMax) {
+            const uint32_t prefix1 = prefix;
+            // pass A: this CTA's counts (keys above the bin, keys in it) -> one atomic
+            // reservation of list slots per CTA (a single hot counter would serialise)
+            uint32_t na = 0, ni = 0;
+            for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
+                const uint32_t hb = key_of(p.sumsq[f]) >> 19;
+                na += hb > prefix1;
+                ni += hb == prefix1;
             }
-            __syncthreads();
-            slot0 = s_sel[3];
-        }
-        // pass B: append the bin's keys with their flat index, in flat order
-        for (int64_t fb = f0; fb < f1 && ni_cta; fb += kThreads) {
-            const int64_t f = fb + threadIdx.x;
-            uint32_t key = 0;
-            bool in = false;
-            if (f < f1) {
-                key = key_of(p.sumsq[f]);
-                in = (key >> 19) == prefix1;
-            }
-            uint64_t tot;
-            const uint32_t ex = (uint32_t)block_excl_scan(in ? 1u : 0u, s_warp, tot);
-            const uint32_t slot = slot0 + ex;
-            if (in && slot < (uint32_t)kCandMax) p.cand[slot] = make_uint2(key, (uint32_t)f);
-            slot0 += (uint32_t)tot;
-        }
-        grid_barrier(p.bar, nbar++);
-        PTRACE(6);
-        const uint32_t nc = __ldcg(p.bar + 16);
-        if (nc <= (uint32_t)kCandMax) {
-            for (uint32_t i0 = threadIdx.x; i0 < nc; i0 += 8 * kThreads) {  // 8 independent loads in flight
-                uint2 c[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) c[u] = i0 + u * kThreads < nc ? __ldcg(p.cand + i0 + u * kThreads) : uint2{};
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (i0 + u * kThreads < nc) {
-                        s_hist[i0 + u * kThreads] = c[u].x;
-                        s_f[i0 + u * kThreads] = c[u].y;
-                    }
-            }
-            __syncthreads();
-            for (int pass = 0; pass < 2 && r < bincnt; ++pass) {  // key bits 18..9, then 8..0
-                const int w = pass == 0 ? 10 : 9;
-                const int nshift = shift - w;
-                for (int i = threadIdx.x; i < (1 << w); i += kThreads) s_h2[i] = 0;
-                __syncthreads();
-                for (uint32_t ib = 0; ib < nc; ib += kThreads) {
-                    const uint32_t i = ib + threadIdx.x;
-                    const uint32_t key = i < nc ? s_hist[i] : 0u;
-                    const bool in = i < nc && (key >> shift) == prefix;
-                    const uint32_t bin = (key >> nshift) & ((1u << w) - 1u);
-                    const uint32_t im = __ballot_sync(0xffffffffu, in);
-                    if (!im) continue;
-                    const int l0 = __ffs(im) - 1;
-                    const uint32_t b0 = __shfl_sync(0xffffffffu, bin, l0);
-                    if (__all_sync(0xffffffffu, !in || bin == b0)) {  // a warp of ties adds once
-                        if (lane == l0) atomicAdd(&s_h2[b0], (uint32_t)__popc(im));
-                    } else if (in) {
-                        atomicAdd(&s_h2[bin], 1u);
-                    }
+            uint32_t slot0, ni_cta;
+            {
+                uint64_t tot;
+                block_excl_scan(((uint64_t)na << 32) | ni, s_warp, tot);
+                ni_cta = (uint32_t)tot;
+                if (threadIdx.x == 0) {
+                    p.cta_cnt[2 * blockIdx.x] = (uint32_t)(tot >> 32);
+                    s_sel[3] = (uint32_t)tot ? atomicAdd(p.bar + 16, (uint32_t)tot) : 0u;
                 }
                 __syncthreads();
-                select_bin<false>(s_h2, 1 << w, r, s_warp, s_sel);
-                prefix = (prefix << w) | s_sel[0];
-                above += s_sel[1];
-                bincnt = s_sel[2];
-                shift = nshift;
-                r = k - above;
+                slot0 = s_sel[3];
             }
-            PTRACE(7);
-            // (above, tie) counts of every block before this CTA's range
-            uint64_t cnt = 0;
-            for (int c = threadIdx.x; c < (int)blockIdx.x; c += kThreads) cnt += (uint64_t)__ldcg(p.cta_cnt + 2 * c) << 32;
-            for (uint32_t i = threadIdx.x; i < nc; i += kThreads) {
-                if ((int64_t)s_f[i] >= f0) continue;
-                const uint32_t kk = s_hist[i] >> shift;
-                cnt += kk > prefix ? (uint64_t)1 << 32 : (kk == prefix ? 1u : 0u);
+            // pass B: append the bin's keys with their flat index, in flat order
+            for (int64_t fb = f0; fb < f1 && ni_cta; fb += kThreads) {
+                const int64_t f = fb + threadIdx.x;
+                uint32_t key = 0;
+                bool in = false;
+                if (f < f1) {
+                    key = key_of(p.sumsq[f]);
+                    in = (key >> 19) == prefix1;
+                }
+                uint64_t tot;
+                const uint32_t ex = (uint32_t)block_excl_scan(in ? 1u : 0u, s_warp, tot);
+                const uint32_t slot = slot0 + ex;
+                if (in && slot < (uint32_t)kCandMax) p.cand[slot] = make_uint2(key, (uint32_t)f);
+                slot0 += (uint32_t)tot;
             }
-            uint64_t tot;
-            block_excl_scan(cnt, s_warp, tot);
-            pre = tot;
-            have_pre = true;
+            grid_barrier(p.bar, nbar++);
+            PTRACE(6);
+            const uint32_t nc = __ldcg(p.bar + 16);  // == bincnt
+            {
+                for (uint32_t i0 = threadIdx.x; i0 < nc; i0 += 8 * kThreads) {  // 8 independent loads in flight
+                    uint2 c[8];
+    #pragma unroll
+                    for (int u = 0; u < 8; ++u) c[u] = i0 + u * kThreads < nc ? __ldcg(p.cand + i0 + u * kThreads) : uint2{};
+    #pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (i0 + u * kThreads < nc) {
+                            s_hist[i0 + u * kThreads] = c[u].x;
+                            s_f[i0 + u * kThreads] = c[u].y;
+                        }
+                }
+                __syncthreads();
+                for (int pass = 0; pass < 2 && r < bincnt; ++pass) {  // key bits 18..9, then 8..0
+                    const int w = pass == 0 ? 10 : 9;
+                    const int nshift = shift - w;
+                    for (int i = threadIdx.x; i < (1 << w); i += kThreads) s_h2[i] = 0;
+                    __syncthreads();
+                    for (uint32_t ib = 0; ib < nc; ib += kThreads) {
+                        const uint32_t i = ib + threadIdx.x;
+                        const uint32_t key = i < nc ? s_hist[i] : 0u;
+                        const bool in = i < nc && (key >> shift) == prefix;
+                        const uint32_t bin = (key >> nshift) & ((1u << w) - 1u);
+                        const uint32_t im = __ballot_sync(0xffffffffu, in);
+                        if (!im) continue;
+                        const int l0 = __ffs(im) - 1;
+                        const uint32_t b0 = __shfl_sync(0xffffffffu, bin, l0);
+                        if (__all_sync(0xffffffffu, !in || bin == b0)) {  // a warp of ties adds once
+                            if (lane == l0) atomicAdd(&s_h2[b0], (uint32_t)__popc(im));
+                        } else if (in) {
+                            atomicAdd(&s_h2[bin], 1u);
+                        }
+                    }
+                    __syncthreads();
+                    select_bin<false>(s_h2, 1 << w, r, s_warp, s_sel);
+                    prefix = (prefix << w) | s_sel[0];
+                    above += s_sel[1];
+                    bincnt = s_sel[2];
+                    shift = nshift;
+                    r = k - above;
+                }
+                PTRACE(7);
+                // (above, tie) counts of every block before this CTA's range
+                uint64_t cnt = 0;
+                for (int c = threadIdx.x; c < (int)blockIdx.x; c += kThreads) cnt += (uint64_t)__ldcg(p.cta_cnt + 2 * c) << 32;
+                for (uint32_t i = threadIdx.x; i < nc; i += kThreads) {
+                    if ((int64_t)s_f[i] >= f0) continue;
+                    const uint32_t kk = s_hist[i] >> shift;
+                    cnt += kk > prefix ? (uint64_t)1 << 32 : (kk == prefix ? 1u : 0u);
+                }
+                uint64_t tot;
+                block_excl_scan(cnt, s_warp, tot);
+                pre = tot;
+                have_pre = true;
+    }
         } else {
-            // the boundary bin overflowed the list (heavy ties): global refinement rounds
+            // the boundary bin does not fit the list (large N or heavy ties): global
+            // refinement rounds (decided from the global histogram, before any pass)
             for (int i = threadIdx.x; i < kH2; i += kThreads) s_hist[i] = 0;
             __syncthreads();
             for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
