@@ -162,9 +162,10 @@ BSR_API bsr_status_t bsr_decompress(const bsr_t *A, void *X_out, void *stream);
  * `dy_dtype`.  accumulate = 0 overwrites dW, 1 adds to it.  Block rows and
  * blocks that were pruned contribute nothing and are never read.  `prec`
  * selects the arithmetic (see bsr_prec_t): FP32 accepts f32 or bf16 operands;
- * TF32 needs f32 values and f32 dY and b in {32, 64}; BF16 needs bf16 values
- * and bf16 dY and b in {16, 32, 64}; both tensor-core paths need N a multiple
- * of 128.  Otherwise BSR_ERR_UNSUPPORTED. */
+ * TF32 needs f32 values and f32 dY and b in {16, 32, 64} (b = 16: two blocks
+ * share each 128-byte tf32 swizzle row, span kernel only); BF16 needs bf16
+ * values and bf16 dY and b in {16, 32, 64}; both tensor-core paths need N a
+ * multiple of 128.  Otherwise BSR_ERR_UNSUPPORTED. */
 BSR_API bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dW,
                        int32_t accumulate, int32_t prec, void *ws, size_t ws_bytes, void *stream);
 

@@ -382,9 +382,6 @@ bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t
                 return fail(BSR_ERR_UNSUPPORTED, "%s tensor-core path needs %s values and dY",
                             prec == BSR_PREC_TF32 ? "TF32" : "BF16", prec == BSR_PREC_TF32 ? "fp32" : "bf16");
             if (A->b < 16) return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs b >= 16 (b=%d)", A->b);
-            if (prec == BSR_PREC_TF32 && A->b < 32)
-                return fail(BSR_ERR_UNSUPPORTED, "TF32 tensor-core path needs b >= 32 (b=%d): MN-major tf32 operands "
-                            "need 128-byte block rows", A->b);
             if (N % 128 != 0) return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs N %% 128 == 0 (N=%lld)", (long long)N);
             if (A->K / A->b > 65535)
                 return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs K/b < 65536 (K/b=%lld)", (long long)(A->K / A->b));

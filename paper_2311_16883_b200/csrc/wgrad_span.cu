@@ -151,36 +151,6 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 
 // TMA loads.  CG = 2: the .cta_group::2 form signals the LEADER CTA's mbarrier
 // (the peer bit of the barrier address cleared), which expects both CTAs' bytes.
-template <int CG>
-__device__ __forceinline__ void tma_3d(const CUtensorMap *tm, uint32_t bar, uint32_t dst, int x, int y, int z) {
-    if constexpr (CG == 2)
-        asm volatile(
-            "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-                dst),
-            "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(bar & 0xFEFFFFFFu)
-            : "memory");
-    else
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-                dst),
-            "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(bar)
-            : "memory");
-}
-template <int CG>
-__device__ __forceinline__ void tma_4d(const CUtensorMap *tm, uint32_t bar, uint32_t dst, int x, int y, int z, int w) {
-    if constexpr (CG == 2)
-        asm volatile(
-            "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
-                dst),
-            "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(bar & 0xFEFFFFFFu)
-            : "memory");
-    else
-        asm volatile(
-            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
-                dst),
-            "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(bar)
-            : "memory");
-}
 
 // The same loads issued by one elected lane of a converged warp whose operands are
 // warp-uniform (no per-lane address waterfall in front of the UTMALDG).
@@ -199,23 +169,6 @@ __device__ __forceinline__ void tma_3d_e(const CUtensorMap *tm, uint32_t bar, ui
             "@p cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n}\n" ::"r"(
                 dst),
             "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(bar)
-            : "memory");
-}
-template <int CG>
-__device__ __forceinline__ void tma_4d_e(const CUtensorMap *tm, uint32_t bar, uint32_t dst, int w) {
-    if constexpr (CG == 2)
-        asm volatile(
-            "{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\n"
-            "@p cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {0, 0, 0, %2}], [%3];\n}\n" ::"r"(
-                dst),
-            "l"(reinterpret_cast<uint64_t>(tm)), "r"(w), "r"(bar & 0xFEFFFFFFu)
-            : "memory");
-    else
-        asm volatile(
-            "{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\n"
-            "@p cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {0, 0, 0, %2}], [%3];\n}\n" ::"r"(
-                dst),
-            "l"(reinterpret_cast<uint64_t>(tm)), "r"(w), "r"(bar)
             : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx_e(uint64_t *bar, uint32_t bytes) {
@@ -297,15 +250,20 @@ struct Cfg {
     static constexpr int A_SBO = KGROUP * 128;
     static constexpr int A_KSTEP = UK * 128;
     static constexpr uint32_t A_LAYOUT = TF32 ? 1u : 2u;  // SW128_32B / SW128
-    // B = X blocks, each [atom][B rows][BW bytes]; blocks BLOCK_BYTES apart
-    static constexpr int BW = (B * ES < 128) ? B * ES : 128;
-    static constexpr int B_ATOMS = B * ES / BW;
+    // B = X blocks, each [atom][B rows][BW bytes]; blocks BLOCK_BYTES apart.
+    // PAIR (tf32, b = 16: 64-byte block rows): MN-major tf32 operands exist only in
+    // 128-byte swizzle rows, so two adjacent blocks of a span share one atom
+    // [B rows][128 B] (left / right half); the loaders place them there.
+    static constexpr bool PAIR = TF32 && B * ES == 64;
+    static constexpr int BW = PAIR ? 128 : (B * ES < 128) ? B * ES : 128;
+    static constexpr int B_ATOMS = PAIR ? 1 : B * ES / BW;
     static constexpr int BLOCK_BYTES = B * B * ES;
+    static constexpr int GRAN = PAIR ? 2 : 1;  // blocks per span granule (times CG)
     static constexpr int B_LBO = B * BW;
     static constexpr int B_SBO = KGROUP * BW;
     static constexpr int B_KSTEP = UK * BW;
     static constexpr uint32_t B_LAYOUT = TF32 ? 1u : BW == 128 ? 2u : BW == 64 ? 4u : 6u;
-    static_assert(!TF32 || BW == 128, "tf32 MN-major operands need 128-byte block rows (b >= 32)");
+    static_assert(!TF32 || B * ES >= 64, "tf32 MN-major operands need 128-byte rows (b >= 16, blocks paired)");
     static constexpr int MAXCB = 256 / B;  // blocks per MMA (N <= 256)
     static constexpr int MAXJ = 512 / B;   // blocks per kcol range (TMEM columns)
 };
@@ -326,7 +284,7 @@ struct Spans {
     uint32_t w[2];  // MMA word per chunk: 1 << 31 | len << 16 | first TMEM column (0: no MMA)
     int f[2], len[2];
 };
-template <int B, int CG>
+template <int B, int CG, int GRAN = 1>
 __device__ __forceinline__ Spans row_spans(uint32_t mk, int nchunk, int cb) {
     Spans sp;
 #pragma unroll
@@ -339,7 +297,7 @@ __device__ __forceinline__ Spans row_spans(uint32_t mk, int nchunk, int cb) {
         if (!cm) continue;
         int f = __ffs(cm) - 1;
         int len = 32 - __clz(cm) - f;
-        if (CG == 2 && (len & 1)) {
+        while (len % (GRAN * CG)) {  // whole granules: each CTA holds len/CG blocks, paired for tf32 b = 16
             if (f + len < cb) {
                 ++len;
             } else {
@@ -371,9 +329,7 @@ __device__ __forceinline__ uint32_t block_smem_off(uint32_t o) {
 
 template <int KIND, int B, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
-    wgrad_span_kernel(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_v1,
-                      const __grid_constant__ CUtensorMap tm_v2, const __grid_constant__ CUtensorMap tm_v4,
-                      const __grid_constant__ CUtensorMap tm_v8, Params p) {
+    wgrad_span_kernel(const __grid_constant__ CUtensorMap tm_dy, Params p) {
     using C = Cfg<KIND, B>;
     // full-barrier arrivals per phase: the producer (+ dY bytes), the 128 loader threads'
     // cp.async completions, and for a pair the peer's relay
@@ -411,10 +367,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 1 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_dy)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v1)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v2)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v4)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_v8)) : "memory");
         for (int i = 0; i < 2; ++i) {
             mbar_init(plan_full + i, 1);
             mbar_init(plan_empty + i, CG == 2 && rank != 0 ? 6 : 5);  // producer, 4 loader warps (+ peer relay)
@@ -549,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t mk = uni(rec.y);
                 const int bs = (int)uni(rec.z);
                 const int row = (int)uni(rec.x);
-                const Spans sp = row_spans<B, CG>(mk, p.nchunk, cb);
+                const Spans sp = row_spans<B, CG, C::GRAN>(mk, p.nchunk, cb);
                 uint32_t bytes = (uint32_t)(CG * C::SLAB);
                 (void)bs;
                 SCLK(te);
@@ -688,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint4 rec = s_plan[buf * 32 + r];
                     const uint32_t mk = rec.y;
                     const int bs = (int)rec.z;
-                    const Spans sp = row_spans<B, CG>(mk, p.nchunk, cb);
+                    const Spans sp = row_spans<B, CG, C::GRAN>(mk, p.nchunk, cb);
                     mbar_wait(empty + stage, phase ^ 1u, 4, (uint32_t)stage);
                     const uint32_t xb = smem0 + (uint32_t)stage * p.stage_bytes + C::SLAB;
                     const int h0 = sp.len[0] / CG, h1 = sp.len[1] / CG;
@@ -701,8 +653,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const bool kept = J < nbJ && ((mk >> J) & 1u);
                         const int idx = kept ? bs + __popc(mk & ((1u << J) - 1u)) : 0;
                         const uint8_t *src = p.values + (int64_t)idx * C::BLOCK_BYTES + off * 16;
-                        const uint32_t dst = xb + (uint32_t)((c * cbh + j) * C::BLOCK_BYTES) +
-                                             block_smem_off<KIND, B>((uint32_t)off * 16u);
+                        uint32_t dst;
+                        if constexpr (C::PAIR) {  // block j: half (j & 1) of atom j / 2, 64-byte block rows
+                            const uint32_t o = (uint32_t)off * 16u, L = (uint32_t)(j >> 1) * (B * 128u) +
+                                                                         (o / 64u) * 128u + (uint32_t)(j & 1) * 64u + o % 64u;
+                            dst = xb + (uint32_t)(c * cbh * C::BLOCK_BYTES) + (L ^ (((L >> 7) & 3u) << 5));
+                        } else {
+                            dst = xb + (uint32_t)((c * cbh + j) * C::BLOCK_BYTES) +
+                                  block_smem_off<KIND, B>((uint32_t)off * 16u);
+                        }
                         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                                      "r"(kept ? 16 : 0)
                                      : "memory");
@@ -808,7 +767,7 @@ static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms, int want_cg) {
         pl.kr_blocks = (nbc + pl.nkr - 1) / pl.nkr;
         pl.nchunk = (pl.kr_blocks + C::MAXCB - 1) / C::MAXCB;
         pl.cb = (pl.kr_blocks + pl.nchunk - 1) / pl.nchunk;
-        if (pl.cg == 2 && (pl.cb & 1)) ++pl.cb;
+        while (pl.cb % (C::GRAN * pl.cg)) ++pl.cb;
         pl.stage_bytes = (uint32_t)((C::SLAB + pl.nchunk * (pl.cb / pl.cg) * C::BLOCK_BYTES + 1023) & ~1023);
         pl.stages = std::min(kMaxStages, (int)((kSmemBudget - kFixedSmem) / pl.stage_bytes));
         if (pl.stages >= 3 || maxJ <= 2) break;
@@ -851,8 +810,7 @@ static void dbg_setup() {
 #endif
 
 template <int KIND, int B, int CG>
-static cudaError_t launch_cg(const Plan &pl, const CUtensorMap &tm_dy, const CUtensorMap *tm_v, const Params &p,
-                             cudaStream_t stream) {
+static cudaError_t launch_cg(const Plan &pl, const CUtensorMap &tm_dy, const Params &p, cudaStream_t stream) {
 #ifdef SPAN_DBGBUF
     dbg_setup();
 #endif
@@ -872,7 +830,7 @@ static cudaError_t launch_cg(const Plan &pl, const CUtensorMap &tm_dy, const CUt
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, tm_dy, tm_v[0], tm_v[1], tm_v[2], tm_v[3], p);
+    e = cudaLaunchKernelEx(&cfg, kern, tm_dy, p);
     count_launch();
     return e;
 }
@@ -891,26 +849,12 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     const CUtensorMapSwizzle sw128 = C::TF32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
     // dY as (column within a 128-byte atom, row, atom): one box = the 128-column x
     // B-row slab of one block row, atom-major in shared memory
-    CUtensorMap tm_dy, tm_v[4];
+    CUtensorMap tm_dy;
     const cuuint64_t dy_dims[3] = {(cuuint64_t)C::ATOM_E, (cuuint64_t)M, (cuuint64_t)(N / C::ATOM_E)};
     const cuuint64_t dy_str[2] = {(cuuint64_t)N * C::ES, 128};
     const cuuint32_t dy_box[3] = {(cuuint32_t)C::ATOM_E, (cuuint32_t)B, (cuuint32_t)C::A_ATOMS};
     cudaError_t e = make_map(&tm_dy, dY, dt, 3, dy_dims, dy_str, dy_box, sw128);
     if (e != cudaSuccess) return e;
-    // values as (element within an atom row, block row, atom, block): one box = one
-    // stored block; block index nnzb is out of bounds and loads zeros
-    const cuuint64_t v_dims[4] = {(cuuint64_t)(C::BW / C::ES), (cuuint64_t)B, (cuuint64_t)C::B_ATOMS, (cuuint64_t)nnzb};
-    const cuuint64_t v_str[3] = {(cuuint64_t)B * C::ES, (cuuint64_t)C::BW, (cuuint64_t)C::BLOCK_BYTES};
-    cuuint32_t v_box[4] = {(cuuint32_t)(C::BW / C::ES), (cuuint32_t)B, (cuuint32_t)C::B_ATOMS, 1u};
-    const CUtensorMapSwizzle swb = C::TF32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
-                                   : C::BW == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
-                                   : C::BW == 64   ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                   : CU_TENSOR_MAP_SWIZZLE_32B;
-    for (int i = 0; i < 4; ++i) {  // boxes of 1, 2, 4, 8 consecutive blocks
-        v_box[3] = 1u << i;
-        e = make_map(&tm_v[i], values, dt, 4, v_dims, v_str, v_box, swb);
-        if (e != cudaSuccess) return e;
-    }
     Params p{};
     p.rowptr = rowptr;
     p.colidx = colidx;
@@ -928,8 +872,7 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     p.stage_bytes = pl.stage_bytes;
     p.mode = pl.nsplit > 1 ? 3 : accumulate ? 1 : 0;
     p.out = pl.nsplit > 1 ? ws : dW;
-    e = pl.cg == 2 ? launch_cg<KIND, B, 2>(pl, tm_dy, tm_v, p, stream)
-                   : launch_cg<KIND, B, 1>(pl, tm_dy, tm_v, p, stream);
+    e = pl.cg == 2 ? launch_cg<KIND, B, 2>(pl, tm_dy, p, stream) : launch_cg<KIND, B, 1>(pl, tm_dy, p, stream);
     if (e != cudaSuccess) return e;
     e = cudaGetLastError();
     if (e != cudaSuccess || pl.nsplit == 1) return e;
@@ -951,7 +894,7 @@ size_t wgrad_span_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
         for (int cg = 1; cg <= 2; ++cg)                                          \
             ns = std::max(ns, span::plan_for<KD, B_>(M, K, N, span::kSplitSMs, cg).nsplit); \
     }
-    WS_CASE(1, 16) WS_CASE(1, 32) WS_CASE(1, 64) WS_CASE(0, 32) WS_CASE(0, 64)
+    WS_CASE(1, 16) WS_CASE(1, 32) WS_CASE(1, 64) WS_CASE(0, 16) WS_CASE(0, 32) WS_CASE(0, 64)
 #undef WS_CASE
     return ns > 1 ? (size_t)ns * K * N * sizeof(float) : 0;
 }
@@ -966,7 +909,7 @@ cudaError_t launch_wgrad_span(const int32_t *rowptr, const int32_t *colidx, cons
     if (kind == KD && b == B_)                                                                                    \
         return span::launch_t<KD, B_>(rowptr, colidx, values, nnzb, M, K, dY, N, dW, accumulate, static_cast<float *>(ws), \
                                       stream);
-    SP_CASE(0, 32) SP_CASE(0, 64) SP_CASE(1, 16) SP_CASE(1, 32) SP_CASE(1, 64)
+    SP_CASE(0, 16) SP_CASE(0, 32) SP_CASE(0, 64) SP_CASE(1, 16) SP_CASE(1, 32) SP_CASE(1, 64)
 #undef SP_CASE
     return cudaErrorInvalidValue;
 }

@@ -1113,7 +1113,8 @@ size_t wgrad_tc_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
 // MMA per short run, while the span kernel's CTA pairs and dense-padded
 // N <= 256 MMAs win (S12 fc2 bf16 b=16: 124 vs 200 us; B24 fc2 b=32: 2.38 vs
 // 3.92 ms f32/tf32, 1.45 vs 2.91 ms bf16).  BSRP_WGRAD=runs|span forces one.
-static bool use_runs_kernel(int b, int64_t K) {
+static bool use_runs_kernel(int kind, int b, int64_t K) {
+    if (kind == 0 && b == 16) return false;  // tf32 b = 16: only the span kernel pairs blocks into 128-byte rows
     const char *e = std::getenv("BSRP_WGRAD");
     if (e && std::string(e) == "span") return false;
     if (e && std::string(e) == "runs") return true;
@@ -1123,7 +1124,7 @@ static bool use_runs_kernel(int b, int64_t K) {
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
                             int kind, int64_t M, int64_t K, int b, const void *dY, int64_t N, float *dW,
                             int accumulate, void *ws, cudaStream_t stream) {
-    if (!use_runs_kernel(b, K))
+    if (!use_runs_kernel(kind, b, K))
         return launch_wgrad_span(rowptr, colidx, values, nnzb, kind, M, K, b, dY, N, dW, accumulate, ws, stream);
     if (!values || nnzb == 0) {  // no stored block: dW = 0 (or unchanged)
         return accumulate ? cudaSuccess : cudaMemsetAsync(dW, 0, (size_t)K * N * sizeof(float), stream);

@@ -38,8 +38,9 @@ def wgrad_kernel(request, monkeypatch):
 
 
 def tc_supported(prec, b):
-    """TF32 MN-major operands need 128-byte block rows: b >= 32 (include/bsrprune.h)."""
-    return not (prec == "tf32" and b < 32)
+    """Both tensor-core paths take b in {16, 32, 64}; tf32 b = 16 pairs two blocks per
+    128-byte swizzle row (span kernel, include/bsrprune.h)."""
+    return b >= 16
 
 
 def run_tc(M, K, N, b, k, prec, family="gelu", seed=0, accumulate=False):
@@ -48,7 +49,7 @@ def run_tc(M, K, N, b, k, prec, family="gelu", seed=0, accumulate=False):
         with pytest.raises(bp.BsrError) as ei:
             bp.wgrad(A, to_torch(synth.grad_out(M, N, seed)), prec=prec)
         assert ei.value.status == 3  # BSR_ERR_UNSUPPORTED
-        pytest.skip("tf32 needs b >= 32 (rejected with BSR_ERR_UNSUPPORTED, as checked)")
+        pytest.skip("tensor cores need b >= 16 (rejected with BSR_ERR_UNSUPPORTED, as checked)")
     X = synth.activation(family, M, K, seed)
     dY = synth.grad_out(M, N, seed)
     if prec == "bf16":

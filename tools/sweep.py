@@ -86,7 +86,7 @@ def timed(fn, sets, reps):
 def prec_for(dtype, b):
     if dtype == torch.bfloat16:
         return "bf16" if b >= 16 else "fp32"
-    return "tf32" if b >= 32 else "fp32"
+    return "tf32" if b >= 16 else "fp32"
 
 
 def sweep_c3(out, hbm, bf16_tf, nsets=3, reps=6):
