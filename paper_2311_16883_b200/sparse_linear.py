@@ -62,7 +62,7 @@ def _default_prec(dtype: torch.dtype, block: int, out_features: int) -> str:
         return "fp32"  # the tensor-core paths need N % 128 == 0
     if dtype == torch.bfloat16:
         return "bf16"
-    return "tf32" if block >= 32 else "fp32"
+    return "tf32" if block >= 16 else "fp32"  # b = 16: tf32 blocks paired per swizzle row (span kernel)
 
 
 def sparse_linear(x: torch.Tensor, weight: torch.Tensor, bias=None, sparsity: float = 0.5, block: int = 16,
