@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -15,6 +16,13 @@
 namespace bsrp {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int pdl_flags() {
+    static const int f = [] {
+        const char *e = std::getenv("BSRP_PDL");
+        return e ? (int)std::strtol(e, nullptr, 0) : kPdlDefault;
+    }();
+    return f;
+}
 }  // namespace bsrp
 
 namespace {

@@ -62,4 +62,12 @@ __device__ __forceinline__ void grid_barrier(uint32_t *counter, uint32_t index) 
     __syncthreads();
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with
+// launch_pdl() may start while its stream predecessor drains; it must call
+// pdl_wait() before its first global-memory access (the wait returns once the
+// predecessor grid has completed and its writes are visible).  pdl_trigger()
+// lets the successor's CTAs be scheduled before this grid exits.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace bsrp

@@ -4,10 +4,36 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace bsrp {
 
 // Process-wide count of kernels this library has launched (bsr_kernel_launches).
 void count_launch(uint64_t n = 1);
+
+// PDL launches.  pdl_flags() = env BSRP_PDL as a bit mask (0: plain stream order):
+//   1 prune triggers before its pack phase, 2 wgrad triggers at its start,
+//   4 wgrad triggers at its epilogue, 8 split-K reduce triggers at its start,
+//   16 / 32 / 64 PDL attribute on the wgrad / reduce / decompress launches.
+constexpr int kPdlDefault = 1 | 4 | 16 | 32 | 64;  // measured best; bit 8 was slower
+int pdl_flags();
+// Launch `kern` with programmatic stream serialization: the kernel MUST call
+// pdl_wait() (common.cuh) before touching global memory.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(bool on, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = on ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Workspace layout of bsr_prune (byte offsets; all 256-aligned).
 struct PruneWs {

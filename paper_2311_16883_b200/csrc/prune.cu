@@ -52,6 +52,7 @@ struct PruneParams {
     int32_t *slot;
     uint32_t *bar, *hist1, *hist2, *hist3, *cta_cnt;
     uint2 *cand;  // [kCandMax] (key, flat index) of the boundary bin's blocks
+    int pdl_trig;   // 1: trigger the PDL successor before the pack phase
     int presummed;  // 1: block sums already in `sumsq` (act_sumsq_kernel); phase 1 skips X
 };
 
@@ -482,6 +483,7 @@ __global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
     scan_and_index(p, f0, f1, pre, prefix, shift, r, s_warp);
     PTRACE(4);
     // ---------------- phase 4: copy kept blocks (raw integer vectors)
+    if (p.pdl_trig) pdl_trigger();  // the next kernel (launched with PDL) may start its prologue
     pack_kept<ES, B>(p, u0, u1);
     __syncthreads();
     PTRACE(5);
@@ -828,6 +830,7 @@ __global__ void __launch_bounds__(256) decompress_kernel(const int32_t *__restri
                                                          const int32_t *__restrict__ colidx,
                                                          const void *__restrict__ values, int64_t K, int64_t nbc,
                                                          int64_t units, int64_t upr, void *__restrict__ Xout) {
+    pdl_wait();  // launched with PDL: no global access before the predecessor completes
     using G_ = Geo<ES, B>;
     using V = typename G_::V;
     const int lane = threadIdx.x & 31;
@@ -961,6 +964,7 @@ cudaError_t launch_prune(const void *X, int64_t M, int64_t K, int b, int es, int
                          int32_t *colidx, void *values, void *ws, cudaStream_t stream, int presummed) {
     PruneParams p{};
     p.presummed = presummed;
+    p.pdl_trig = pdl_flags() & 1;
     p.X = X;
     p.K = K;
     p.nbr = M / b;
@@ -1033,10 +1037,10 @@ cudaError_t launch_decompress(const int32_t *rowptr, const int32_t *colidx, cons
 #define CALL(ES_, B_) ([&]() {                                                                   \
         int64_t upr = units_per_row<ES_, B_>(nbc), units = nbr * upr;                          \
         int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((units + 7) / 8, 148 * 16));      \
-        decompress_kernel<ES_, B_><<<(unsigned)blocks, 256, 0, stream>>>(rowptr, colidx, values, K, nbc, \
-                                                                         units, upr, Xout);    \
+        cudaError_t e_ = launch_pdl(pdl_flags() & 64, decompress_kernel<ES_, B_>, dim3((unsigned)blocks), dim3(256), 0, stream, \
+                                    rowptr, colidx, values, K, nbc, units, upr, Xout);                    \
         count_launch();                                                                        \
-        return cudaGetLastError();                                                             \
+        return e_ != cudaSuccess ? e_ : cudaGetLastError();                                    \
     }())
     if (es == 4) {
         BSRP_DISPATCH_B(4, b, CALL)

@@ -233,6 +233,7 @@ struct Params {
     int chunk_steps;             // steps of one metadata chunk (rowptr + colidx staged in smem)
     int sa;                      // shared-memory A ring stages
     uint32_t a_col0;             // first TMEM column of the A buffers
+    int pdl_trig;                // PDL successor trigger: 0 none, 1 at start, 2 at the epilogue
 };
 
 template <int KIND, int B>
@@ -437,6 +438,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *s_tmem;
+    // PDL: the prologue above overlapped the predecessor's tail; no global
+    // access before this point.  The split-K reduce may be scheduled now.
+    pdl_wait();
+    if (p.pdl_trig == 1) pdl_trigger();
 
     if (warp == 3) {
         // ------------------------------------------------ step planner
@@ -856,6 +861,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // its own workspace slice (summed afterwards in split order:
         // deterministic); mode 1 adds into dW (accumulate, one split).
         mbar_wait_sleep(accfull, 0);
+        if (p.pdl_trig == 2) pdl_trigger();
         tc_fence_after();
         if (threadIdx.x == 128) TRACE(203);
         const int ew = warp - 4;
@@ -912,7 +918,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Each thread owns float4 column blocks; up to 16 split loads are issued ahead
 // of the (ordered) adds so the L2-resident partials stream at full rate.
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4 *__restrict__ ws, float4 *__restrict__ dW,
-                                                            int64_t n4, int nsplit, int accumulate) {
+                                                            int64_t n4, int nsplit, int accumulate, int trig) {
+    if (trig) pdl_trigger();
+    pdl_wait();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
         float4 a = accumulate ? dW[i] : make_float4(0.f, 0.f, 0.f, 0.f);
         for (int s = 0; s < nsplit; s += 16) {  // up to 16 independent loads in flight, then ordered adds
@@ -1059,20 +1067,22 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     p.chunk_steps = pl.chunk_steps;
     p.ws = ws;
     p.mode = pl.nsplit > 1 ? 3 : accumulate ? 1 : 0;
+    p.pdl_trig = (pdl_flags() & 2) ? 1 : (pdl_flags() & 4) ? 2 : 0;
     auto kern = wgrad_tc_kernel<KIND, B>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((N / 128) * pl.nkr * pl.nsplit);
-    kern<<<grid, kThreads, pl.smem, stream>>>(tm_dy, tm_val, tm_dw, tm_ws, p);
+    e = launch_pdl(pdl_flags() & 16, kern, dim3(grid), dim3(kThreads), (size_t)pl.smem, stream, tm_dy, tm_val, tm_dw, tm_ws, p);
+    if (e != cudaSuccess) return e;
     count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess || pl.nsplit == 1) return e;
     const int64_t n4 = K * N / 4;
     const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 8));
-    splitk_reduce_kernel<<<rgrid, 256, 0, stream>>>(reinterpret_cast<const float4 *>(ws),
-                                                    reinterpret_cast<float4 *>(dW), n4, pl.nsplit, accumulate);
+    e = launch_pdl(pdl_flags() & 32, splitk_reduce_kernel, dim3(rgrid), dim3(256), 0, stream, reinterpret_cast<const float4 *>(ws),
+                   reinterpret_cast<float4 *>(dW), n4, (int)pl.nsplit, accumulate, (pdl_flags() & 8) ? 1 : 0);
     count_launch();
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace tc
@@ -1083,10 +1093,11 @@ cudaError_t launch_splitk_reduce(const float *ws, float *dW, int64_t n, int nspl
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t n4 = n / 4;
     const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 8));
-    tc::splitk_reduce_kernel<<<rgrid, 256, 0, stream>>>(reinterpret_cast<const float4 *>(ws),
-                                                        reinterpret_cast<float4 *>(dW), n4, nsplit, accumulate);
+    cudaError_t e = launch_pdl(pdl_flags() & 32, tc::splitk_reduce_kernel, dim3(rgrid), dim3(256), 0, stream,
+                               reinterpret_cast<const float4 *>(ws), reinterpret_cast<float4 *>(dW), n4, nsplit,
+                               accumulate, (pdl_flags() & 8) ? 1 : 0);
     count_launch();
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 static size_t wgrad_runs_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
