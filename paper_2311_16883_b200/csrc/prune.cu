@@ -825,6 +825,11 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const void *X, int64_t K, in
 }
 
 // BSR -> dense: every output row segment written once (zeros or the block).
+// The warp's unit covers G consecutive block columns of one block row; the
+// row's stored columns are scanned 32 at a time with one coalesced colidx load
+// per chunk (instead of a dependent binary search per lane), each hit parks its
+// stored index in a per-warp shared-memory slot.  Rows are copied RD at a time
+// (16 in flight per lane for the wide blocks).
 template <int ES, int B>
 __global__ void __launch_bounds__(256) decompress_kernel(const int32_t *__restrict__ rowptr,
                                                          const int32_t *__restrict__ colidx,
@@ -833,31 +838,40 @@ __global__ void __launch_bounds__(256) decompress_kernel(const int32_t *__restri
     pdl_wait();  // launched with PDL: no global access before the predecessor completes
     using G_ = Geo<ES, B>;
     using V = typename G_::V;
-    const int lane = threadIdx.x & 31;
+    constexpr int RD = (B < 16) ? B : 16;
+    __shared__ int s_pos[256 / 32][G_::G];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int j = lane / G_::LPB, sub = lane % G_::LPB;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t u = wg; u < units; u += nwg) {
-        const int64_t I = u / upr, J = (u % upr) * G_::G + j;
-        if (J >= nbc) continue;
-        // binary search of J among the (ascending) stored columns of row I
-        int lo = __ldg(rowptr + I), hi = __ldg(rowptr + I + 1);
-        while (lo < hi) {
-            int mid = (lo + hi) >> 1;
-            if (__ldg(colidx + mid) < J) lo = mid + 1; else hi = mid;
+        const int64_t I = u / upr;
+        const int Jb = (int)((u % upr) * G_::G);
+        const int64_t J = Jb + j;
+        if (lane < G_::G) s_pos[wid][lane] = -1;
+        __syncwarp();
+        const int rb = __ldg(rowptr + I), re = __ldg(rowptr + I + 1);
+        for (int c = rb; c < re; c += 32) {
+            const int idx = c + lane;
+            const int col = idx < re ? __ldg(colidx + idx) : 0x7fffffff;
+            if (col >= Jb && col < Jb + G_::G) s_pos[wid][col - Jb] = idx;
+            if (__shfl_sync(0xffffffffu, col, 31) >= Jb + G_::G) break;  // colidx ascending: past the unit
         }
-        const bool present = lo < __ldg(rowptr + I + 1) && __ldg(colidx + lo) == J;
+        __syncwarp();
+        const int lo = s_pos[wid][j];
+        __syncwarp();  // slots are re-initialised by the next unit
+        if (J >= nbc) continue;
         const int64_t rs = K / G_::EPV;
         V *dst = reinterpret_cast<V *>(Xout) + (I * B) * rs + (J * B) / G_::EPV + sub;
-        if (present) {
+        if (lo >= 0) {
             const V *src = reinterpret_cast<const V *>(values) + (int64_t)lo * (B * B / G_::EPV) + sub;
 #pragma unroll
-            for (int r0 = 0; r0 < B; r0 += G_::R) {
-                V v[G_::R];
+            for (int r0 = 0; r0 < B; r0 += RD) {
+                V v[RD];
 #pragma unroll
-                for (int rr = 0; rr < G_::R; ++rr) v[rr] = ld_stream(src + (r0 + rr) * G_::LPB);
+                for (int rr = 0; rr < RD; ++rr) v[rr] = ld_stream(src + (r0 + rr) * G_::LPB);
 #pragma unroll
-                for (int rr = 0; rr < G_::R; ++rr) __stcs(dst + (r0 + rr) * rs, v[rr]);
+                for (int rr = 0; rr < RD; ++rr) __stcs(dst + (r0 + rr) * rs, v[rr]);
             }
         } else {
             V z{};

@@ -915,21 +915,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // dW (+)= sum over splits of the partial tiles, in split order (deterministic).
-// Each thread owns float4 column blocks; up to 16 split loads are issued ahead
-// of the (ordered) adds so the L2-resident partials stream at full rate.
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4 *__restrict__ ws, float4 *__restrict__ dW,
-                                                            int64_t n4, int nsplit, int accumulate, int trig) {
+// Each thread owns float4 column blocks; up to 8 split loads are issued ahead
+// of the (ordered) adds so the L2-resident partials stream at full rate.  <= 64
+// registers: 4 CTAs per SM, so the C2 grid (576 CTAs) runs in one wave.
+__global__ void __launch_bounds__(256, 4) splitk_reduce_kernel(const float4 *__restrict__ ws, float4 *__restrict__ dW,
+                                                               int64_t n4, int nsplit, int accumulate, int trig) {
     if (trig) pdl_trigger();
     pdl_wait();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
         float4 a = accumulate ? dW[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s = 0; s < nsplit; s += 16) {  // up to 16 independent loads in flight, then ordered adds
-            float4 v[16];
+        for (int s = 0; s < nsplit; s += 8) {  // up to 8 independent loads in flight, then ordered adds
+            float4 v[8];
 #pragma unroll
-            for (int u = 0; u < 16; ++u)
+            for (int u = 0; u < 8; ++u)
                 if (s + u < nsplit) v[u] = __ldcs(ws + (size_t)(s + u) * n4 + i);
 #pragma unroll
-            for (int u = 0; u < 16; ++u)
+            for (int u = 0; u < 8; ++u)
                 if (s + u < nsplit) {
                     a.x += v[u].x; a.y += v[u].y; a.z += v[u].z; a.w += v[u].w;
                 }
@@ -1078,7 +1079,7 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     e = cudaGetLastError();
     if (e != cudaSuccess || pl.nsplit == 1) return e;
     const int64_t n4 = K * N / 4;
-    const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 8));
+    const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 4));
     e = launch_pdl(pdl_flags() & 32, splitk_reduce_kernel, dim3(rgrid), dim3(256), 0, stream, reinterpret_cast<const float4 *>(ws),
                    reinterpret_cast<float4 *>(dW), n4, (int)pl.nsplit, accumulate, (pdl_flags() & 8) ? 1 : 0);
     count_launch();
@@ -1092,7 +1093,7 @@ cudaError_t launch_splitk_reduce(const float *ws, float *dW, int64_t n, int nspl
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t n4 = n / 4;
-    const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 8));
+    const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 4));
     cudaError_t e = launch_pdl(pdl_flags() & 32, tc::splitk_reduce_kernel, dim3(rgrid), dim3(256), 0, stream,
                                reinterpret_cast<const float4 *>(ws), reinterpret_cast<float4 *>(dW), n4, nsplit,
                                accumulate, (pdl_flags() & 8) ? 1 : 0);

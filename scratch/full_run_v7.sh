@@ -8,7 +8,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 for k in wgrad_tc prune_kernel decompress splitk_reduce; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 -o gpurun_out/prof_$k python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_$k.log 2>&1; tail -1 gpurun_out/ncu_$k.log
 done
-for k in wgrad_tc prune_kernel; do
+for k in wgrad_tc prune_kernel decompress splitk_reduce; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 -o gpurun_out/prof_bf16_$k python bench.py --dtype bf16 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_bf16_$k.log 2>&1; tail -1 gpurun_out/ncu_bf16_$k.log
 done
 ls gpurun_out
