@@ -21,7 +21,11 @@
  *    NULL = legacy default stream) and is asynchronous: results are valid once
  *    the stream reaches that point.  Asynchronous device faults surface at the
  *    caller's next synchronisation.  No call performs a device->host copy, so
- *    every call is CUDA-graph capturable.
+ *    every call is CUDA-graph capturable.  bsr_wgrad's kernels and
+ *    bsr_decompress are launched with programmatic stream serialization (PDL):
+ *    they may become resident while the preceding kernel on `stream` drains,
+ *    but read and write nothing before it has completed, so stream-order
+ *    semantics are unchanged (env BSRP_PDL=0 turns the attribute off).
  *  * Arguments are validated on the host before anything is enqueued; on any
  *    non-BSR_OK return nothing has been written.  bsr_last_error() then holds a
  *    human-readable reason for the calling thread.
