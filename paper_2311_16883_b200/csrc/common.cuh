@@ -46,18 +46,18 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
 // Grid-wide barrier for a cooperatively launched (co-resident) grid.  The
 // counter is monotonic within one launch and zeroed before the launch;
 // barrier number `i` (0-based) completes when (i+1)*gridDim.x arrivals exist.
+// Release/acquire (the CUTLASS generic-barrier pattern): bar.sync orders the
+// CTA's writes before thread 0's red.release, thread 0's ld.acquire orders the
+// other CTAs' writes before the closing bar.sync -- no full fences.
 __device__ __forceinline__ void grid_barrier(uint32_t *counter, uint32_t index) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(counter, 1u);
+        asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(counter), "r"(1u) : "memory");
         const uint32_t target = (index + 1u) * gridDim.x;
         uint32_t spins = 0;
         while (ld_acquire_gpu(counter) < target) {
-            __nanosleep(32);
             if (++spins > (1u << 26)) __trap();  // workspace not zero-filled / corrupted: fail, do not hang
         }
-        __threadfence();
     }
     __syncthreads();
 }
