@@ -76,7 +76,7 @@ struct Geo {
     static constexpr int EPV = VB / ES;                      // elements per vector
     static constexpr int LPB = B / EPV;                      // lanes per block row
     static constexpr int G = kWarp / LPB;                    // blocks per warp unit
-    static constexpr int R = (B < 8) ? B : 8;                // rows in flight per lane
+    static constexpr int R = (B < 16) ? (B < 8 ? B : 8) : 16;  // rows in flight per lane
     using V = typename Vec<VB>::T;
 };
 
@@ -244,7 +244,7 @@ __device__ unsigned long long g_ptrace[2048][8];
 #endif
 
 template <int ES, int B>
-__global__ void __launch_bounds__(kThreads, 2) prune_kernel(PruneParams p) {
+__global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_kernel(PruneParams p) {
     using G_ = Geo<ES, B>;
     __shared__ uint32_t s_hist[kH1];  // level-1 histogram, then the candidate keys
     __shared__ uint32_t s_f[kCandMax];  // candidate flat indices
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1) prune_small_kernel(PruneParams p)
 // keep keys (>> shift) > T and the first `r` keys == T in flat order.  The block
 // sums of squares are already in the workspace (bsr_select_hist level 0).
 template <int ES, int B>
-__global__ void __launch_bounds__(kThreads, 2) prune_apply_kernel(PruneParams p, uint32_t T, int shift, uint32_t r) {
+__global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_apply_kernel(PruneParams p, uint32_t T, int shift, uint32_t r) {
     using G_ = Geo<ES, B>;
     __shared__ uint64_t s_warp[32];
     __shared__ uint32_t s_sel[4];
