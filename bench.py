@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--b", type=int, default=None)
     ap.add_argument("--keep", type=float, default=None)
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of CUDA-graph replays")
+    ap.add_argument("--order", choices=["pwd", "pdw"], default="pwd",
+                    help="kernel order inside a step: prune-wgrad-decompress or prune-decompress-wgrad")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
@@ -282,7 +284,7 @@ def run_native(a):
     dWs = [torch.empty(K, N, dtype=torch.float32, device=dev) for _ in range(NSETS)]
     Xds = [torch.empty(M, K, dtype=tdt, device=dev) for _ in range(NSETS)]
 
-    phases = ["prune", "wgrad", "decompress"]
+    phases = ["prune", "wgrad", "decompress"] if a.order == "pwd" else ["prune", "decompress", "wgrad"]
 
     def phase_fn(j, p):
         if p == "prune":
