@@ -839,7 +839,7 @@ __global__ void __launch_bounds__(256) decompress_kernel(const int32_t *__restri
     using G_ = Geo<ES, B>;
     using V = typename G_::V;
     constexpr int RD = (B < 16) ? B : 16;
-    __shared__ int s_pos[256 / 32][G_::G];
+    __shared__ int s_pos[256 / 32][G_::G];  // B >= 16 lookup slots
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int j = lane / G_::LPB, sub = lane % G_::LPB;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -848,18 +848,33 @@ __global__ void __launch_bounds__(256) decompress_kernel(const int32_t *__restri
         const int64_t I = u / upr;
         const int Jb = (int)((u % upr) * G_::G);
         const int64_t J = Jb + j;
-        if (lane < G_::G) s_pos[wid][lane] = -1;
-        __syncwarp();
-        const int rb = __ldg(rowptr + I), re = __ldg(rowptr + I + 1);
-        for (int c = rb; c < re; c += 32) {
-            const int idx = c + lane;
-            const int col = idx < re ? __ldg(colidx + idx) : 0x7fffffff;
-            if (col >= Jb && col < Jb + G_::G) s_pos[wid][col - Jb] = idx;
-            if (__shfl_sync(0xffffffffu, col, 31) >= Jb + G_::G) break;  // colidx ascending: past the unit
+        int lo;
+        if constexpr (B >= 16) {
+            if (lane < G_::G) s_pos[wid][lane] = -1;
+            __syncwarp();
+            const int rb = __ldg(rowptr + I), re = __ldg(rowptr + I + 1);
+            // entries with col >= Jb start no earlier than re - (nbc - Jb) (columns are unique and ascending)
+            for (int c = max(rb, re - (int)(nbc - Jb)); c < re; c += 32) {
+                const int idx = c + lane;
+                const int col = idx < re ? __ldg(colidx + idx) : 0x7fffffff;
+                if (col >= Jb && col < Jb + G_::G) s_pos[wid][col - Jb] = idx;
+                if (__shfl_sync(0xffffffffu, col, 31) >= Jb + G_::G) break;  // colidx ascending: past the unit
+            }
+            __syncwarp();
+            lo = s_pos[wid][j];
+            __syncwarp();  // slots are re-initialised by the next unit
+        } else {
+            // small blocks: G = 16..32 columns per unit, one per lane group -- a
+            // per-lane binary search keeps the lookups independent (measured
+            // faster than the chunk scan for b = 4 at 1-4 GiB, profiles/r01_sweep_v7)
+            int l = __ldg(rowptr + I), h = __ldg(rowptr + I + 1);
+            const int he = h;
+            while (l < h) {
+                const int mid = (l + h) >> 1;
+                if (__ldg(colidx + mid) < J) l = mid + 1; else h = mid;
+            }
+            lo = (J < nbc && l < he && __ldg(colidx + l) == J) ? l : -1;
         }
-        __syncwarp();
-        const int lo = s_pos[wid][j];
-        __syncwarp();  // slots are re-initialised by the next unit
         if (J >= nbc) continue;
         const int64_t rs = K / G_::EPV;
         V *dst = reinterpret_cast<V *>(Xout) + (I * B) * rs + (J * B) / G_::EPV + sub;
