@@ -25,7 +25,7 @@
  *    bsr_decompress are launched with programmatic stream serialization (PDL):
  *    they may become resident while the preceding kernel on `stream` drains,
  *    but read and write nothing before it has completed, so stream-order
- *    semantics are unchanged (env BSRP_PDL=0 turns the attribute off).
+ *    semantics are unchanged (bsr_set_pdl(0) turns the attribute off).
  *  * Arguments are validated on the host before anything is enqueued; on any
  *    non-BSR_OK return nothing has been written.  bsr_last_error() then holds a
  *    human-readable reason for the calling thread.
@@ -36,7 +36,8 @@
  *    Base pointers must be 16-byte aligned and K * sizeof(elem) a multiple of
  *    16 bytes (vectorised rows).
  *  * The library is reentrant; the only global state is the thread-local
- *    error string and per-device kernel attributes set once.
+ *    error string, per-device kernel attributes set once, the launch counter
+ *    and the PDL mask of bsr_set_pdl (an atomic; default = measured best).
  */
 #ifndef BSRPRUNE_H
 #define BSRPRUNE_H
@@ -67,14 +68,33 @@ typedef enum {
 typedef enum { BSR_DT_F32 = 0, BSR_DT_BF16 = 1 } bsr_dtype_t;
 
 /* Arithmetic of bsr_wgrad (reading R9 in DESIGN.md):
- *   BSR_PREC_FP32 : fp32 operands, fp32 FFMA with round-to-nearest, fixed
- *                   summation order (deterministic).  Graded at relative
- *                   Frobenius error <= 1e-5 against the fp64 oracle.
+ *   BSR_PREC_FP32 : FP32 grade, graded at relative Frobenius error <= 1e-5
+ *                   against the fp64 oracle; deterministic.  With f32 values
+ *                   and f32 dY, b in {32, 64} and N % 128 == 0 it runs on the
+ *                   tcgen05 tensor cores as 3xTF32 (each operand split into a
+ *                   tf32 head and an fp32 tail, three MMAs per k step, the two
+ *                   correction products in their own TMEM accumulator, at most
+ *                   1536 rows per accumulator chain, split partials summed with
+ *                   round-to-nearest; reading R17); otherwise fp32 FFMA with
+ *                   round-to-nearest in a fixed summation order (f32 or bf16
+ *                   operands).
  *   BSR_PREC_TF32 : tcgen05 tensor cores, kind::tf32 on fp32 operands, fp32
  *                   accumulation in TMEM.  Graded at <= 5e-3.
  *   BSR_PREC_BF16 : tcgen05 tensor cores, kind::f16 on bf16 operands (X values
  *                   and dY both bf16), fp32 accumulation in TMEM.  <= 5e-3. */
 typedef enum { BSR_PREC_FP32 = 0, BSR_PREC_TF32 = 1, BSR_PREC_BF16 = 2 } bsr_prec_t;
+
+/* dW kernel family for bsr_wgrad_algo (bsr_wgrad = BSR_ALGO_AUTO):
+ *   AUTO    : the measured best for the shape: tensor cores when
+ *             the precision allows; the per-run tcgen05 kernel for K/b < 64, the
+ *             CTA-pair span kernel for K/b >= 64 (tf32/bf16) and for tf32 b = 16;
+ *             FP32 FFMA when no tensor-core kernel supports the combination.
+ *   TC_RUNS : per-run tcgen05 kernel (tf32/bf16 b >= 32 or bf16 b = 16; FP32
+ *             grade b in {32, 64}).
+ *   TC_SPAN : CTA-pair span kernel (tf32/bf16, b >= 16; not the FP32 grade).
+ *   SIMT    : fp32 FFMA (any b, f32 or bf16 operands; BSR_PREC_FP32 only).
+ * A combination the chosen family does not implement is BSR_ERR_UNSUPPORTED. */
+typedef enum { BSR_ALGO_AUTO = 0, BSR_ALGO_TC_RUNS = 1, BSR_ALGO_TC_SPAN = 2, BSR_ALGO_SIMT = 3 } bsr_algo_t;
 
 /* A Block Sparse Row matrix.  The struct itself lives in host
  * memory; the three arrays are device memory owned by the caller.
@@ -172,6 +192,19 @@ BSR_API bsr_status_t bsr_decompress(const bsr_t *A, void *X_out, void *stream);
  * multiple of 128.  Otherwise BSR_ERR_UNSUPPORTED. */
 BSR_API bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dW,
                        int32_t accumulate, int32_t prec, void *ws, size_t ws_bytes, void *stream);
+
+/* bsr_wgrad with an explicit kernel family (bsr_algo_t): same operation, same
+ * grading; used by the parity tests to cover every kernel on every shape.  The
+ * workspace query bsr_wgrad_workspace_bytes covers every family. */
+BSR_API bsr_status_t bsr_wgrad_algo(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dW,
+                                    int32_t accumulate, int32_t prec, int32_t algo, void *ws, size_t ws_bytes,
+                                    void *stream);
+
+/* Programmatic-dependent-launch mask of this process (bit meanings in
+ * csrc/launch.h; 0 = plain stream order).  Returns the previous mask.  Results
+ * are bit-identical for every mask (tests/test_pdl_gpu.py); only the overlap
+ * of a kernel's prologue with its predecessor's tail changes. */
+BSR_API uint32_t bsr_set_pdl(uint32_t mask);
 
 /* ---- cross-rank global top-k ----------------------------
  * Under data parallelism each rank holds a shard of X's rows.  bsr_prune keeps

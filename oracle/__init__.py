@@ -24,6 +24,11 @@ other than itself:
   decompress                  equals X * kron(mask, ones) (numpy).
   wgrad / wgrad_entries       keep=1 -> numpy X^T @ dY; any keep ->
                               (X*mask)^T @ dY (numpy matmul); linearity.
+  wgrad_masked                the same definition with a library matmul as its
+                              one step: decompress (the C oracle) then numpy's
+                              fp64 (X*mask)^T @ dY.  Used where the quadruple
+                              loop is too slow (B24 shards, 59 GFLOP); pinned
+                              to wgrad within 1e-12 (tests/test_oracle.py).
   prune_per_sample            SPEC's per-sample examples (golden
                               fixture), brute force per sample, count
                               exactness per sample, numpy segment norms.
@@ -221,6 +226,21 @@ def wgrad_entries(rowptr, colidx, values, M: int, K: int, b: int, dY: np.ndarray
                                      dY.shape[1], _ptr(rows), _ptr(cols), rows.size, _ptr(out)),
            "wgrad_entries")
     return out
+
+
+def _as_f64(a: np.ndarray) -> np.ndarray:
+    """fp32 values, or bf16 stored as uint16 bit patterns (exact 16-bit shift)."""
+    if a.dtype == np.uint16 or a.dtype == np.int16:
+        return (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    return a.astype(np.float64)
+
+
+def wgrad_masked(rowptr, colidx, values, M: int, K: int, b: int, dY: np.ndarray) -> np.ndarray:
+    """fp64 dW = (X*mask)^T . dY (BJ): the dense masked X rebuilt by
+    the C oracle's decompress (O6), then ONE library matmul in fp64.  Same
+    definition as `wgrad`, summed by BLAS instead of the quadruple loop."""
+    Xm = _as_f64(decompress(rowptr, colidx, values, M, K, b))
+    return Xm.T @ _as_f64(np.ascontiguousarray(dY))
 
 
 def wgrad_rect(rowptr, colidx, values, M: int, K: int, br: int, bc: int, dY: np.ndarray) -> np.ndarray:

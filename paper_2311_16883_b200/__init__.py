@@ -17,10 +17,10 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import BsrError, DT_BF16, DT_F32, PREC
+from ._lib import ALGO, BsrError, DT_BF16, DT_F32, PREC
 
 __all__ = ["BSR", "BsrError", "prune", "decompress", "wgrad", "block_sumsq", "num_blocks", "keep_count",
-           "storage_bytes", "workspace", "version", "SparseLinear", "sparse_linear", "prune_global",
+           "storage_bytes", "workspace", "version", "set_pdl", "SparseLinear", "sparse_linear", "prune_global",
            "RowBSR", "prune_rows", "decompress_rows", "wgrad_rows", "act_prune"]
 
 _DT = {torch.float32: DT_F32, torch.bfloat16: DT_BF16}
@@ -95,19 +95,46 @@ def storage_bytes(M: int, b: int, k: int, dtype=torch.float32) -> int:
 _WS: dict = {}
 
 
-def workspace(nbytes: int, device: torch.device, kind: str = "wgrad") -> torch.Tensor:
-    """Cached device workspace of at least nbytes, one per (device, kind).
+def _stream_obj(device: torch.device, stream=None):
+    return torch.cuda.current_stream(device) if stream is None else stream
 
-    The prune workspace is zero-filled when allocated and used for nothing else:
-    bsr_prune needs a zero-filled workspace on first use and leaves it that way
-    (include/bsrprune.h)."""
-    key = (device.type, device.index, kind)
+
+def workspace(nbytes: int, device: torch.device, kind: str = "wgrad", stream=None) -> torch.Tensor:
+    """Cached device workspace of at least nbytes, one per (device, kind, stream).
+
+    Keyed on the launch stream so that calls in flight on different streams never
+    share a workspace (the prune keeps its grid-barrier counter and histograms
+    there, the dW its split-K partials).  The buffer is allocated -- and, for the
+    prune, zero-filled -- ON that stream, so the first launch is ordered after the
+    fill.  bsr_prune needs a zero-filled workspace on first use and leaves it that
+    way (include/bsrprune.h), so the prune workspace is used for nothing else."""
+    s = _stream_obj(device, stream)
+    key = (device.type, device.index, kind, s.cuda_stream)
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
-        alloc = torch.zeros if kind == "prune" else torch.empty
-        ws = alloc(max(nbytes, 256), dtype=torch.uint8, device=device)
+        with torch.cuda.stream(s):
+            alloc = torch.zeros if kind == "prune" else torch.empty
+            ws = alloc(max(nbytes, 256), dtype=torch.uint8, device=device)
         _WS[key] = ws
     return ws
+
+
+def _check_out_bsr(out: "BSR", M: int, K: int, b: int, k: int, dtype: torch.dtype, device) -> None:
+    """The caller-supplied output BSR must match the call exactly (the kernel writes
+    k colidx entries, k*b*b values and M/b+1 rowptr entries)."""
+    if (out.M, out.K, out.b) != (M, K, b):
+        raise ValueError(f"out BSR is for M={out.M} K={out.K} b={out.b}, the call has M={M} K={K} b={b}")
+    for name, t, n, dt in (("rowptr", out.rowptr, M // b + 1, torch.int32), ("colidx", out.colidx, k, torch.int32)):
+        if t.dtype != dt or t.numel() != n or not t.is_contiguous() or t.device != device:
+            raise ValueError(f"out.{name} must be a contiguous {dt} tensor of {n} elements on {device}")
+    v = out.values
+    if v.dtype != dtype or tuple(v.shape) != (k, b, b) or not v.is_contiguous() or v.device != device:
+        raise ValueError(f"out.values must be a contiguous {dtype} tensor of shape ({k}, {b}, {b}) on {device}")
+
+
+def _check_dense_out(t: torch.Tensor, shape, dtype, device, name: str) -> None:
+    if t.dtype != dtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous() or t.device != device:
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor of shape {tuple(shape)} on {device}")
 
 
 def alloc_bsr(M: int, K: int, b: int, k: int, dtype: torch.dtype, device) -> BSR:
@@ -131,9 +158,12 @@ def prune(X: torch.Tensor, b: int, keep: float | None = None, k: int | None = No
         raise ValueError("give exactly one of keep or k")
     if k is None:
         k = keep_count(N, keep)
-    out = out or alloc_bsr(M, K, b, k, X.dtype, X.device)
+    if out is None:
+        out = alloc_bsr(M, K, b, k, X.dtype, X.device)
+    else:
+        _check_out_bsr(out, M, K, b, k, X.dtype, X.device)
     ws_bytes = lib.bsr_prune_workspace_bytes(M, K, b)
-    ws = workspace(ws_bytes, X.device, kind="prune")
+    ws = workspace(ws_bytes, X.device, kind="prune", stream=stream)
     cs = out.c_struct()
     _lib.check(lib.bsr_prune_k(X.data_ptr(), M, K, b, k, _dt(X), ctypes.byref(cs), ws.data_ptr(), ws.numel(),
                                _stream(stream)))
@@ -155,10 +185,14 @@ def act_prune(Z: torch.Tensor, b: int, keep: float | None = None, k: int | None 
         k = keep_count(N, keep)
     if X_out is None:
         X_out = torch.empty_like(Z)
+    else:
+        _check_dense_out(X_out, (M, K), Z.dtype, Z.device, "X_out")
     if out is None:
         out = alloc_bsr(M, K, b, k, Z.dtype, Z.device)
+    else:
+        _check_out_bsr(out, M, K, b, k, Z.dtype, Z.device)
     ws_bytes = lib.bsr_prune_workspace_bytes(M, K, b)
-    ws = workspace(ws_bytes, Z.device, kind="prune")
+    ws = workspace(ws_bytes, Z.device, kind="prune", stream=stream)
     a = {"identity": 0, "gelu": 1}[act]
     _lib.check(lib.bsr_act_block_sumsq(Z.data_ptr(), X_out.data_ptr(), M, K, b, _dt(Z), a, ws.data_ptr(), ws.numel(),
                                        _stream(stream)))
@@ -180,15 +214,22 @@ def block_sumsq(X: torch.Tensor, b: int, stream=None) -> torch.Tensor:
 
 def decompress(A: BSR, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     lib = _lib.load()
-    out = torch.empty((A.M, A.K), dtype=A.dtype, device=A.rowptr.device) if out is None else out
+    if out is None:
+        out = torch.empty((A.M, A.K), dtype=A.dtype, device=A.rowptr.device)
+    else:
+        _check_dense_out(out, (A.M, A.K), A.dtype, A.rowptr.device, "out")
     cs = A.c_struct()
     _lib.check(lib.bsr_decompress(ctypes.byref(cs), out.data_ptr(), _stream(stream)))
     return out
 
 
 def wgrad(A: BSR, dY: torch.Tensor, prec: str = "fp32", out: torch.Tensor | None = None,
-          accumulate: bool = False, stream=None) -> torch.Tensor:
-    """dW = X_bsr^T . dY (K x N fp32) over the kept blocks only."""
+          accumulate: bool = False, stream=None, algo: str = "auto") -> torch.Tensor:
+    """dW = X_bsr^T . dY (K x N fp32) over the kept blocks only.
+
+    prec: "fp32" (FP32 grade, rel-F <= 1e-5: 3xTF32 tensor cores or FFMA), "tf32"
+    or "bf16" (tensor cores, <= 5e-3).  algo: "auto" (the library's per-shape
+    choice), "runs", "span" (the two tcgen05 kernels) or "simt" (FFMA)."""
     lib = _lib.load()
     dY = _cuda2d(dY, "dY")
     if dY.shape[0] != A.M:
@@ -196,14 +237,21 @@ def wgrad(A: BSR, dY: torch.Tensor, prec: str = "fp32", out: torch.Tensor | None
     N = dY.shape[1]
     if out is None:
         out = torch.empty((A.K, N), dtype=torch.float32, device=dY.device)
+    else:
+        _check_dense_out(out, (A.K, N), torch.float32, dY.device, "out")
     p = PREC[prec]
     ws_bytes = lib.bsr_wgrad_workspace_bytes(A.M, A.K, A.b, N, p)
-    ws = workspace(ws_bytes, dY.device) if ws_bytes else None
+    ws = workspace(ws_bytes, dY.device, stream=stream) if ws_bytes else None
     cs = A.c_struct()
-    _lib.check(lib.bsr_wgrad(ctypes.byref(cs), dY.data_ptr(), _dt(dY), N, out.data_ptr(), int(accumulate), p,
-                             ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0,
-                             _stream(stream)))
+    _lib.check(lib.bsr_wgrad_algo(ctypes.byref(cs), dY.data_ptr(), _dt(dY), N, out.data_ptr(), int(accumulate), p,
+                                  ALGO[algo], ws.data_ptr() if ws is not None else None,
+                                  ws.numel() if ws is not None else 0, _stream(stream)))
     return out
+
+
+def set_pdl(mask: int) -> int:
+    """Process-wide programmatic-dependent-launch mask (include/bsrprune.h); returns the old one."""
+    return int(_lib.load().bsr_set_pdl(int(mask)))
 
 
 from .sparse_linear import SparseLinear, sparse_linear  # noqa: E402  (uses the functions above)

@@ -17,10 +17,11 @@ STATUS_NAMES = {0: "BSR_OK", 1: "BSR_ERR_INVALID_ARG", 2: "BSR_ERR_SHAPE", 3: "B
                 4: "BSR_ERR_ALIGNMENT", 5: "BSR_ERR_WORKSPACE", 6: "BSR_ERR_CUDA"}
 DT_F32, DT_BF16 = 0, 1
 PREC = {"fp32": 0, "tf32": 1, "bf16": 2}
+ALGO = {"auto": 0, "runs": 1, "span": 2, "simt": 3}
 
 EXPORTED = ["bsr_num_blocks", "bsr_keep_count", "bsr_storage_bytes", "bsr_prune_workspace_bytes",
             "bsr_wgrad_workspace_bytes", "bsr_prune", "bsr_prune_k", "bsr_block_sumsq", "bsr_decompress",
-            "bsr_wgrad", "bsr_select_hist", "bsr_select_counts", "bsr_prune_threshold", "bsr_rows_keep_per_sample", "bsr_prune_rows_workspace_bytes", "bsr_prune_rows",
+            "bsr_wgrad", "bsr_wgrad_algo", "bsr_set_pdl", "bsr_select_hist", "bsr_select_counts", "bsr_prune_threshold", "bsr_rows_keep_per_sample", "bsr_prune_rows_workspace_bytes", "bsr_prune_rows",
             "bsr_decompress_rows", "bsr_wgrad_rows_workspace_bytes", "bsr_wgrad_rows", "bsr_act_block_sumsq", "bsr_prune_presummed", "bsr_status_string", "bsr_last_error", "bsr_kernel_launches", "bsr_version"]
 
 
@@ -62,6 +63,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "bsr_block_sumsq": (i32, [vp, i64, i64, i32, i32, vp, vp]),
         "bsr_decompress": (i32, [P, vp, vp]),
         "bsr_wgrad": (i32, [P, vp, i32, i64, vp, i32, i32, vp, sz, vp]),
+        "bsr_wgrad_algo": (i32, [P, vp, i32, i64, vp, i32, i32, i32, vp, sz, vp]),
+        "bsr_set_pdl": (ctypes.c_uint32, [ctypes.c_uint32]),
         "bsr_select_hist": (i32, [vp, i64, i64, i32, i32, i32, ctypes.c_uint32, vp, vp, sz, vp]),
         "bsr_select_counts": (i32, [i64, i64, i32, ctypes.c_uint32, i32, vp, vp, sz, vp]),
         "bsr_prune_threshold": (i32, [vp, i64, i64, i32, i32, ctypes.c_uint32, i32, i64, i64, P, vp, sz, vp]),

@@ -2,6 +2,7 @@
 // size queries, error reporting and dispatch to the sm_100a kernels.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -15,14 +16,9 @@
 
 namespace bsrp {
 static std::atomic<uint64_t> g_launches{0};
+static std::atomic<uint32_t> g_pdl{(uint32_t)kPdlDefault};
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
-int pdl_flags() {
-    static const int f = [] {
-        const char *e = std::getenv("BSRP_PDL");
-        return e ? (int)std::strtol(e, nullptr, 0) : kPdlDefault;
-    }();
-    return f;
-}
+int pdl_flags() { return (int)g_pdl.load(std::memory_order_relaxed); }
 }  // namespace bsrp
 
 namespace {
@@ -118,7 +114,8 @@ size_t bsr_prune_workspace_bytes(int64_t M, int64_t K, int32_t b) {
 
 size_t bsr_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec) {
     if (bsr_num_blocks(M, K, b) < 0 || N <= 0) return 0;
-    if (prec == BSR_PREC_FP32) return bsrp::wgrad_simt_ws_bytes(M, K, b, N);
+    if (prec == BSR_PREC_FP32)
+        return std::max(bsrp::wgrad_simt_ws_bytes(M, K, b, N), bsrp::wgrad_x3_ws_bytes(M, K, b, N));
     return bsrp::wgrad_tc_ws_bytes(M, K, b, N);
 }
 
@@ -355,8 +352,16 @@ bsr_status_t bsr_decompress(const bsr_t *A, void *X_out, void *stream) {
                        "bsr_decompress launch");
 }
 
-bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dW, int32_t accumulate,
-                       int32_t prec, void *ws, size_t ws_bytes, void *stream) {
+static bsr_status_t check_wgrad_ws(size_t need, void *ws, size_t ws_bytes, const float *dW, size_t dw_bytes) {
+    if (need && (!ws || ws_bytes < need))
+        return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+    if (need && !aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
+    if (need && overlap(ws, need, dW, dw_bytes)) return fail(BSR_ERR_INVALID_ARG, "workspace overlaps dW");
+    return BSR_OK;
+}
+
+bsr_status_t bsr_wgrad_algo(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dW,
+                            int32_t accumulate, int32_t prec, int32_t algo, void *ws, size_t ws_bytes, void *stream) {
     bsr_status_t st = check_bsr(A);
     if (st != BSR_OK) return st;
     const int esy = elem_size(dy_dtype);
@@ -364,49 +369,61 @@ bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t
     if (N <= 0 || N > (int64_t(1) << 30)) return fail(BSR_ERR_SHAPE, "N=%lld out of range", (long long)N);
     if (!dY || !dW) return fail(BSR_ERR_INVALID_ARG, "dY or dW is NULL");
     if (accumulate != 0 && accumulate != 1) return fail(BSR_ERR_INVALID_ARG, "accumulate must be 0 or 1");
+    if (algo < BSR_ALGO_AUTO || algo > BSR_ALGO_SIMT) return fail(BSR_ERR_INVALID_ARG, "algo %d is not a bsr_algo_t", algo);
     if (!aligned16(dY) || !aligned16(dW)) return fail(BSR_ERR_ALIGNMENT, "dY or dW is not 16-byte aligned");
     if ((N * esy) % 16 != 0 || (N * 4) % 16 != 0)
         return fail(BSR_ERR_ALIGNMENT, "row pitch of dY/dW (N=%lld) is not a multiple of 16 bytes", (long long)N);
     const int esx = elem_size(A->dtype);
-    if (overlap(dW, (size_t)A->K * N * 4, dY, (size_t)A->M * N * esy))
-        return fail(BSR_ERR_INVALID_ARG, "dW overlaps dY");
+    const size_t dw_bytes = (size_t)A->K * N * 4;
+    if (overlap(dW, dw_bytes, dY, (size_t)A->M * N * esy)) return fail(BSR_ERR_INVALID_ARG, "dW overlaps dY");
+    if (A->K / A->b > 65535)
+        return fail(BSR_ERR_UNSUPPORTED, "K/b must stay below 65536 (K/b=%lld)", (long long)(A->K / A->b));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    switch (prec) {
-        case BSR_PREC_FP32: {
-            const size_t need = bsrp::wgrad_simt_ws_bytes(A->M, A->K, A->b, N);
-            if (need && (!ws || ws_bytes < need))
-                return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
-            if (need && !aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
-            if (need && overlap(ws, need, dW, (size_t)A->K * N * 4))
-                return fail(BSR_ERR_INVALID_ARG, "workspace overlaps dW");
-            return cuda_status(bsrp::launch_wgrad_simt(A->rowptr, A->colidx, A->nnzb ? A->values : nullptr, esx, A->M,
-                                                       A->K, A->b, dY, esy, N, dW, accumulate, ws, s),
-                               "bsr_wgrad (fp32) launch");
-        }
-        case BSR_PREC_TF32:
-        case BSR_PREC_BF16: {
-            const int want = prec == BSR_PREC_TF32 ? BSR_DT_F32 : BSR_DT_BF16;
-            if (A->dtype != want || dy_dtype != want)
-                return fail(BSR_ERR_UNSUPPORTED, "%s tensor-core path needs %s values and dY",
-                            prec == BSR_PREC_TF32 ? "TF32" : "BF16", prec == BSR_PREC_TF32 ? "fp32" : "bf16");
-            if (A->b < 16) return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs b >= 16 (b=%d)", A->b);
-            if (N % 128 != 0) return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs N %% 128 == 0 (N=%lld)", (long long)N);
-            if (A->K / A->b > 65535)
-                return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs K/b < 65536 (K/b=%lld)", (long long)(A->K / A->b));
-            const size_t need = bsrp::wgrad_tc_ws_bytes(A->M, A->K, A->b, N);
-            if (need && (!ws || ws_bytes < need))
-                return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
-            if (need && !aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
-            if (need && overlap(ws, need, dW, (size_t)A->K * N * 4))
-                return fail(BSR_ERR_INVALID_ARG, "workspace overlaps dW");
-            return cuda_status(bsrp::launch_wgrad_tc(A->rowptr, A->colidx, A->values, A->nnzb, prec == BSR_PREC_TF32 ? 0 : 1,
+    if (prec == BSR_PREC_FP32) {
+        // FP32 grade: 3xTF32 tensor cores where implemented, else FFMA
+        const bool x3 = A->dtype == BSR_DT_F32 && dy_dtype == BSR_DT_F32 &&
+                        bsrp::wgrad_tc_supported(2, algo == BSR_ALGO_AUTO ? 1 : algo, A->b, A->K, N);
+        if (algo == BSR_ALGO_TC_SPAN || (algo == BSR_ALGO_TC_RUNS && !x3))
+            return fail(BSR_ERR_UNSUPPORTED, "FP32-grade tensor-core dW needs the per-run kernel, f32 values and dY, "
+                                             "b in {32, 64} and N %% 128 == 0");
+        if (x3 && algo != BSR_ALGO_SIMT) {
+            st = check_wgrad_ws(bsrp::wgrad_x3_ws_bytes(A->M, A->K, A->b, N), ws, ws_bytes, dW, dw_bytes);
+            if (st != BSR_OK) return st;
+            return cuda_status(bsrp::launch_wgrad_tc(A->rowptr, A->colidx, A->values, A->nnzb, 2, BSR_ALGO_TC_RUNS,
                                                      A->M, A->K, A->b, dY, N, dW, accumulate, ws, s),
-                               "bsr_wgrad (tensor-core) launch");
+                               "bsr_wgrad (fp32 grade, 3xTF32) launch");
         }
-        default:
-            return fail(BSR_ERR_INVALID_ARG, "prec %d is not a bsr_prec_t", prec);
+        st = check_wgrad_ws(bsrp::wgrad_simt_ws_bytes(A->M, A->K, A->b, N), ws, ws_bytes, dW, dw_bytes);
+        if (st != BSR_OK) return st;
+        return cuda_status(bsrp::launch_wgrad_simt(A->rowptr, A->colidx, A->nnzb ? A->values : nullptr, esx, A->M, A->K,
+                                                   A->b, dY, esy, N, dW, accumulate, ws, s),
+                           "bsr_wgrad (fp32) launch");
     }
+    if (prec != BSR_PREC_TF32 && prec != BSR_PREC_BF16) return fail(BSR_ERR_INVALID_ARG, "prec %d is not a bsr_prec_t", prec);
+    const int want = prec == BSR_PREC_TF32 ? BSR_DT_F32 : BSR_DT_BF16;
+    if (A->dtype != want || dy_dtype != want)
+        return fail(BSR_ERR_UNSUPPORTED, "%s tensor-core path needs %s values and dY", prec == BSR_PREC_TF32 ? "TF32" : "BF16",
+                    prec == BSR_PREC_TF32 ? "fp32" : "bf16");
+    if (algo == BSR_ALGO_SIMT) return fail(BSR_ERR_UNSUPPORTED, "the FFMA kernel implements BSR_PREC_FP32 only");
+    if (A->b < 16) return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs b >= 16 (b=%d)", A->b);
+    if (N % 128 != 0) return fail(BSR_ERR_UNSUPPORTED, "tensor-core path needs N %% 128 == 0 (N=%lld)", (long long)N);
+    const int kind = prec == BSR_PREC_TF32 ? 0 : 1;
+    if (!bsrp::wgrad_tc_supported(kind, algo, A->b, A->K, N))
+        return fail(BSR_ERR_UNSUPPORTED, "tensor-core kernel family %d does not implement %s at b=%d, K=%lld", algo,
+                    prec == BSR_PREC_TF32 ? "tf32" : "bf16", A->b, (long long)A->K);
+    st = check_wgrad_ws(bsrp::wgrad_tc_ws_bytes(A->M, A->K, A->b, N), ws, ws_bytes, dW, dw_bytes);
+    if (st != BSR_OK) return st;
+    return cuda_status(bsrp::launch_wgrad_tc(A->rowptr, A->colidx, A->values, A->nnzb, kind, algo, A->M, A->K, A->b, dY,
+                                             N, dW, accumulate, ws, s),
+                       "bsr_wgrad (tensor-core) launch");
 }
+
+bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dW, int32_t accumulate,
+                       int32_t prec, void *ws, size_t ws_bytes, void *stream) {
+    return bsr_wgrad_algo(A, dY, dy_dtype, N, dW, accumulate, prec, BSR_ALGO_AUTO, ws, ws_bytes, stream);
+}
+
+uint32_t bsr_set_pdl(uint32_t mask) { return bsrp::g_pdl.exchange(mask); }
 
 const char *bsr_status_string(int32_t status) {
     switch (status) {

@@ -11,7 +11,7 @@ namespace bsrp {
 // Process-wide count of kernels this library has launched (bsr_kernel_launches).
 void count_launch(uint64_t n = 1);
 
-// PDL launches.  pdl_flags() = env BSRP_PDL as a bit mask (0: plain stream order):
+// PDL launches.  pdl_flags() = the bsr_set_pdl bit mask (0: plain stream order):
 //   1 prune triggers before its pack phase, 2 wgrad triggers at its start,
 //   4 wgrad triggers at its epilogue, 8 split-K reduce triggers at its start,
 //   16 / 32 / 64 PDL attribute on the wgrad / reduce / decompress launches.
@@ -80,10 +80,13 @@ cudaError_t launch_wgrad_simt(const int32_t *rowptr, const int32_t *colidx, cons
                               int64_t N, float *dW, int accumulate, void *ws, cudaStream_t stream);
 
 // dW = X_bsr^T dY on tcgen05 tensor cores.  kind: 0 = tf32 (fp32 operands),
-// 1 = f16 (bf16 operands).
+// 1 = f16 (bf16 operands), 2 = FP32 grade (3xTF32, fp32 operands).
+// algo: 0 auto, 1 per-run kernel, 2 span kernel (bsr_algo_t).
 size_t wgrad_tc_ws_bytes(int64_t M, int64_t K, int b, int64_t N);
+size_t wgrad_x3_ws_bytes(int64_t M, int64_t K, int b, int64_t N);
+bool wgrad_tc_supported(int kind, int algo, int b, int64_t K, int64_t N);
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values,
-                            int64_t nnzb, int kind, int64_t M, int64_t K, int b, const void *dY,
+                            int64_t nnzb, int kind, int algo, int64_t M, int64_t K, int b, const void *dY,
                             int64_t N, float *dW, int accumulate, void *ws, cudaStream_t stream);
 
 // Span kernel (wgrad_span.cu): dense-padded per-row spans, CTA-pair MMAs.

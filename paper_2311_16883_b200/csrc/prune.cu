@@ -236,12 +236,6 @@ __device__ __forceinline__ void pack_kept(const PruneParams &p, int64_t u0, int6
     }
 }
 
-#ifdef PRUNE_TRACE
-__device__ unsigned long long g_ptrace[2048][8];
-#define PTRACE(i) do { if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); g_ptrace[blockIdx.x][(i)] = t_; } } while (0)
-#else
-#define PTRACE(i) ((void)0)
-#endif
 
 template <int ES, int B>
 __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_kernel(PruneParams p) {
@@ -261,8 +255,6 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_kernel(Prun
     const int64_t f0 = flat_start(u0), f1 = flat_start(u1);
     const int j = lane / G_::LPB, sub = lane % G_::LPB;
     uint32_t nbar = 0;
-
-    PTRACE(0);
     // ---------------- phase 1: block sums of squares + level-1 histogram
     for (int i = threadIdx.x; i < kH1; i += kThreads) s_hist[i] = 0;
     __syncthreads();
@@ -282,9 +274,7 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_kernel(Prun
     __syncthreads();
     for (int i = threadIdx.x; i < kH1; i += kThreads)
         if (s_hist[i]) atomicAdd(p.hist1 + i, s_hist[i]);
-    PTRACE(1);
     grid_barrier(p.bar, nbar++);
-    PTRACE(2);
 
     // ---------------- phase 2: radix select of the k-th largest key
     const uint32_t k = (uint32_t)p.k;
@@ -339,7 +329,6 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_kernel(Prun
                 slot0 += (uint32_t)tot;
             }
             grid_barrier(p.bar, nbar++);
-            PTRACE(6);
             const uint32_t nc = __ldcg(p.bar + 16);  // == bincnt
             {
                 for (uint32_t i0 = threadIdx.x; i0 < nc; i0 += 8 * kThreads) {  // 8 independent loads in flight
@@ -382,7 +371,6 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_kernel(Prun
                     shift = nshift;
                     r = k - above;
                 }
-                PTRACE(7);
                 // (above, tie) counts of every block before this CTA's range
                 uint64_t cnt = 0;
                 for (int c = threadIdx.x; c < (int)blockIdx.x; c += kThreads) cnt += (uint64_t)__ldcg(p.cta_cnt + 2 * c) << 32;
@@ -434,8 +422,6 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_kernel(Prun
             }
         }
     }
-
-    PTRACE(3);
     // ---------------- phase 3: flat-order scan -> slots, colidx, rowptr
     if (!have_pre) {
         uint32_t na = 0, nt = 0;
@@ -481,174 +467,10 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_kernel(Prun
         }
     }
     scan_and_index(p, f0, f1, pre, prefix, shift, r, s_warp);
-    PTRACE(4);
     // ---------------- phase 4: copy kept blocks (raw integer vectors)
     if (p.pdl_trig) pdl_trigger();  // the next kernel (launched with PDL) may start its prologue
     pack_kept<ES, B>(p, u0, u1);
     __syncthreads();
-    PTRACE(5);
-}
-
-// Small-N variant (N <= kSmallN): one grid barrier.  Phase 1 is prune_kernel's
-// (block sums of squares + the global 12-bit first-digit histogram).  After the
-// barrier every CTA reads the histogram, finds the boundary bin, loads ALL N keys
-// from L2 into shared memory and gathers the boundary bin's keys (the
-// candidates) and refines the remaining 19 key bits over them with shared-memory
-// histograms (over all N keys when the bin exceeds kCandCap).  Each
-// CTA then counts the kept / tied blocks before its own flat range itself -- so
-// no refinement or scan barrier.  Same selection rule and outputs as prune_kernel.
-constexpr int64_t kSmallN = 40960;
-constexpr int kCandCap = 8192;
-
-template <int ES, int B>
-__global__ void __launch_bounds__(kThreads, 1) prune_small_kernel(PruneParams p) {
-    using G_ = Geo<ES, B>;
-    extern __shared__ uint32_t s_dyn[];
-    uint32_t *s_key = s_dyn;                                   // [N]
-    uint32_t *s_cand = s_dyn + ((p.N + 3) & ~int64_t(3));      // [kCandCap]
-    __shared__ uint32_t s_hist[kH1];
-    __shared__ uint64_t s_warp[32];
-    __shared__ uint32_t s_sel[4];
-    __shared__ uint32_t s_nc;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kThreads / 32;
-    const int64_t u0 = (int64_t)blockIdx.x * p.units / gridDim.x;
-    const int64_t u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
-    auto flat_start = [&](int64_t u) -> int64_t {
-        return u >= p.units ? p.N : (u / p.upr) * p.nbc + (u % p.upr) * G_::G;
-    };
-    const int64_t f0 = flat_start(u0), f1 = flat_start(u1);
-    const int j = lane / G_::LPB, sub = lane % G_::LPB;
-    const int N = (int)p.N;
-
-    PTRACE(0);
-    // ---------------- phase 1: block sums of squares + level-1 histogram
-    for (int i = threadIdx.x; i < kH1; i += kThreads) s_hist[i] = 0;
-    if (threadIdx.x == 0) s_nc = 0;
-    __syncthreads();
-    for (int64_t u = u0 + wid; u < u1; u += nw) {
-        const int64_t I = u / p.upr, J = (u % p.upr) * G_::G + j;
-        const bool valid = J < p.nbc;
-        float s = block_sumsq_warp<ES, B>(p.X, p.K, I, J, sub, valid);
-        if (valid && sub == 0) {
-            p.sumsq[I * p.nbc + J] = s;
-            atomicAdd(&s_hist[key_of(s) >> 19], 1u);
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kH1; i += kThreads)
-        if (s_hist[i]) atomicAdd(p.hist1 + i, s_hist[i]);
-    PTRACE(1);
-    grid_barrier(p.bar, 0);
-    PTRACE(2);
-
-    // ---------------- phase 2: boundary bin (global histogram), candidates, exact key
-    select_bin(p.hist1, kH1, (uint32_t)p.k, s_warp, s_sel);
-    const uint32_t prefix1 = s_sel[0];
-    uint32_t need = (uint32_t)p.k - s_sel[1];
-    const uint32_t bincnt = s_sel[2];
-    // Self-cleaning workspace: this CTA is done with the histogram and the barrier
-    // counter; the last CTA to get here zeroes them for the next launch.
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_sel[3] = atomicAdd(p.bar + 32, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_sel[3]) {
-        __threadfence();
-        for (int i = threadIdx.x; i < kH1; i += kThreads) p.hist1[i] = 0;
-        if (threadIdx.x == 0) {
-            p.bar[0] = 0;
-            p.bar[32] = 0;
-        }
-    }
-    {  // all keys into shared memory: independent 16-byte loads, several in flight per thread
-        const float4 *src = reinterpret_cast<const float4 *>(p.sumsq);
-        const int n4 = N / 4;
-        for (int i0 = threadIdx.x; i0 < n4; i0 += 4 * kThreads) {
-            float4 v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = i0 + u * kThreads < n4 ? __ldcg(src + i0 + u * kThreads) : float4{};
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (i0 + u * kThreads < n4)
-                    reinterpret_cast<uint4 *>(s_key)[i0 + u * kThreads] =
-                        make_uint4(key_of(v[u].x), key_of(v[u].y), key_of(v[u].z), key_of(v[u].w));
-        }
-        for (int f = n4 * 4 + threadIdx.x; f < N; f += kThreads) s_key[f] = key_of(__ldcg(p.sumsq + f));
-    }
-    __syncthreads();
-    PTRACE(6);
-    for (int fb = 0; fb < N; fb += kThreads) {
-        const int f = fb + threadIdx.x;
-        const uint32_t key = f < N ? s_key[f] : 0u;
-        const bool cand = f < N && (key >> 19) == prefix1;
-        const uint32_t m = __ballot_sync(0xffffffffu, cand);
-        uint32_t base = 0;
-        if (m && lane == 0) base = atomicAdd(&s_nc, (uint32_t)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
-        if (cand && pos < kCandCap) s_cand[pos] = key;
-    }
-    __syncthreads();
-    PTRACE(7);
-    const uint32_t nc = s_nc;  // == bincnt
-    uint32_t prefix = prefix1;
-    int shift = 19;
-    // Refine while the boundary bin is split: 10 + 9 more key bits, histograms in
-    // shared memory over the candidates (or over all keys when the bin is too big
-    // for the candidate buffer); a warp whose keys share one bin adds once.
-    const bool in_cand = nc <= kCandCap;
-    const uint32_t *arr = in_cand ? s_cand : s_key;
-    const int len = in_cand ? (int)nc : N;
-    uint32_t cnt = bincnt;
-    for (int pass = 0; pass < 2 && need < cnt; ++pass) {
-        const int w = pass == 0 ? 10 : 9;
-        const int nshift = shift - w;
-        for (int i = threadIdx.x; i < (1 << w); i += kThreads) s_hist[i] = 0;
-        __syncthreads();
-        for (int fb = 0; fb < len; fb += kThreads) {
-            const int f = fb + threadIdx.x;
-            const uint32_t key = f < len ? arr[f] : 0u;
-            const bool in = f < len && (key >> shift) == prefix;
-            const uint32_t bin = (key >> nshift) & ((1u << w) - 1u);
-            const uint32_t im = __ballot_sync(0xffffffffu, in);
-            if (!im) continue;
-            const int l0 = __ffs(im) - 1;
-            const uint32_t b0 = __shfl_sync(0xffffffffu, bin, l0);
-            if (__all_sync(0xffffffffu, !in || bin == b0)) {
-                if (lane == l0) atomicAdd(&s_hist[b0], (uint32_t)__popc(im));
-            } else if (in) {
-                atomicAdd(&s_hist[bin], 1u);
-            }
-        }
-        __syncthreads();
-        select_bin<false>(s_hist, 1 << w, need, s_warp, s_sel);
-        prefix = (prefix << w) | s_sel[0];
-        need -= s_sel[1];
-        cnt = s_sel[2];
-        shift = nshift;
-        __syncthreads();
-    }
-    const uint32_t r = need;
-    PTRACE(3);
-
-    // ---------------- phase 3: (above, tie) counts before this CTA's range, then its slots
-    uint32_t na = 0, nt = 0;
-    for (int64_t f = threadIdx.x; f < f0; f += kThreads) {
-        const uint32_t kk = s_key[f] >> shift;
-        na += kk > prefix;
-        nt += kk == prefix;
-    }
-    uint64_t pre;
-    block_excl_scan(((uint64_t)na << 32) | nt, s_warp, pre);
-    scan_and_index(p, f0, f1, pre, prefix, shift, r, s_warp);
-    PTRACE(4);
-
-    // ---------------- phase 4: copy kept blocks
-    pack_kept<ES, B>(p, u0, u1);
-    __syncthreads();
-    PTRACE(5);
 }
 
 // Pack with a threshold chosen elsewhere (cross-rank global top-k, select_global.cu):
@@ -920,13 +742,6 @@ static int units_per_row(int64_t nbc) {
     return (int)((nbc + Geo<ES, B>::G - 1) / Geo<ES, B>::G);
 }
 
-// BSRP_PRUNE_SMALL=1 selects the one-barrier small-N kernel (measured no faster
-// than the multi-barrier kernel at C2; kept parity-tested for A/B).
-static bool small_path_enabled() {
-    const char *e = std::getenv("BSRP_PRUNE_SMALL");
-    return e && e[0] == '1';
-}
-
 static int num_sms() {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -947,21 +762,6 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
     }
     // (no per-launch memset: the kernel leaves its workspace header zeroed, see above)
     cudaError_t e = cudaSuccess;
-    if (p.N <= kSmallN && small_path_enabled() && !p.presummed) {
-        const size_t smem = (size_t)((p.N + 3) & ~int64_t(3)) * 4 + (size_t)kCandCap * 4;
-        e = cudaFuncSetAttribute(prune_small_kernel<ES, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        int occ = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, prune_small_kernel<ES, B>, kThreads, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) return cudaErrorLaunchOutOfResources;
-        int64_t grid = std::min<int64_t>((int64_t)occ * num_sms(), kMaxGrid);
-        grid = std::min<int64_t>(grid, std::max<int64_t>(1, (p.units + kThreads / 32 - 1) / (kThreads / 32)));
-        void *args[] = {&p};
-        count_launch();
-        return cudaLaunchCooperativeKernel((const void *)prune_small_kernel<ES, B>, dim3((unsigned)grid),
-                                           dim3(kThreads), args, smem, stream);
-    }
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, prune_kernel<ES, B>, kThreads, 0);
     if (e != cudaSuccess) return e;
@@ -971,10 +771,6 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
     grid = std::min<int64_t>(grid, std::max<int64_t>(1, (p.units + kThreads / 32 - 1) / (kThreads / 32)));
     void *args[] = {&p};
     count_launch();
-#ifdef PRUNE_NONCOOP
-    prune_kernel<ES, B><<<(unsigned)grid, kThreads, 0, stream>>>(p);
-    return cudaGetLastError();
-#endif
     return cudaLaunchCooperativeKernel((const void *)prune_kernel<ES, B>, dim3((unsigned)grid), dim3(kThreads),
                                        args, 0, stream);
 }

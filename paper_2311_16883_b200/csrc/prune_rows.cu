@@ -440,6 +440,12 @@ cudaError_t launch_prune_rows(const void *X, int64_t M, int64_t K, int b, int es
         count_launch();                                                                                           \
         const int64_t ns_ = S * (K / B_);                                                                         \
         const size_t smem_ = ns_ <= rows::kSmemKeys ? (size_t)ns_ * 4 : 0;                                        \
+        /* 48 KB of keys + the static shared arrays exceed the default 48 KB dynamic limit: opt in */            \
+        if (smem_) {                                                                                              \
+            const cudaError_t ea_ = cudaFuncSetAttribute(rows::rows_select_kernel<ES_, B_>,                         \
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_); \
+            if (ea_ != cudaSuccess) return ea_;                                                                   \
+        }                                                                                                         \
         rows::rows_select_kernel<ES_, B_><<<(unsigned)(M / S), rows::kThreads, smem_, stream>>>(                   \
             static_cast<const uint8_t *>(X), K, S, ks, sumsq, rowptr, colidx, static_cast<uint8_t *>(values));     \
         count_launch();                                                                                           \

@@ -55,26 +55,6 @@ constexpr int kColCap = 2048;    // colidx entries of one plan group staged in s
 constexpr int kFixedSmem = 1024 /*align*/ + kBarBytes + 2 * 32 * 16 /*plan*/ + 36 * 4 + 2 * kColCap;
 constexpr int kSplitSMs = 148;
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
-#ifdef SPAN_TRACE
-__device__ unsigned long long g_strace[160][16];
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define STRACE(i) (g_strace[blockIdx.x][(i)] = gtimer())
-#define SCLK(v) const long long v = clock64()
-#define SADD(acc, v) (acc += clock64() - (v))
-#define SSET(i, val) (g_strace[blockIdx.x][(i)] = (unsigned long long)(val))
-#else
-#define STRACE(i) ((void)0)
-#define SCLK(v) ((void)0)
-#define SADD(acc, v) ((void)0)
-#define SSET(i, val) ((void)0)
-#endif
-#ifndef SPAN_MODE
-#define SPAN_MODE 0  // dev experiments only: bit 0 = no MMAs, bit 1 = no X-block TMAs, bit 2 = no dY TMAs
-#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -99,25 +79,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-#ifdef SPAN_DBGBUF
-__device__ unsigned *g_dbg;  // host-mapped: the timeout record survives the trap
-__device__ __forceinline__ void dbg_timeout(uint32_t what, uint32_t a, uint32_t b) {
-    unsigned *d = g_dbg;
-    if (d) {
-        const unsigned i = atomicAdd(d, 1u);
-        if (i < 64) {
-            volatile unsigned *e = d + 4 + 4 * i;
-            e[0] = blockIdx.x;
-            e[1] = ((threadIdx.x >> 5) << 16) | what;
-            e[2] = a;
-            e[3] = b;
-        }
-        __threadfence_system();
-    }
-}
-#else
 __device__ __forceinline__ void dbg_timeout(uint32_t, uint32_t, uint32_t) {}
-#endif
 // Bounded wait: a pipeline bug traps (launch error) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, uint32_t what = 0, uint32_t info = 0) {
     uint32_t spins = 0;
@@ -351,7 +313,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint16_t *s_col = reinterpret_cast<uint16_t *>(s_rp + 36);                  // [kColCap]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) STRACE(0);
     const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
     int t = blockIdx.x / CG;
     const int ntp = (int)(p.N / (128 * CG));
@@ -412,7 +373,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
-    if (threadIdx.x == 0) STRACE(1);
 
     const uint32_t smem0 = smem_u32(smem);
     if (warp == 3) {
@@ -453,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // Warm L2 one plan group ahead of the producer: this CTA's dY slabs of the
             // group's rows (tensor-map prefetch) and the group's stored blocks (shared
             // by every n tile of these rows: one CTA pair pulls them from HBM).
-            if (!(SPAN_MODE & 32)) {
+            {
                 if (mask)
                     asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
                                      reinterpret_cast<uint64_t>(&tm_dy)),
@@ -487,13 +447,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         const int cb = p.cb;
-        long long t_plan = 0, t_empty = 0, t_tma = 0, n_rows = 0;
-        (void)t_plan; (void)t_empty; (void)t_tma; (void)n_rows;
         for (int g = 0;; ++g) {
             const int buf = g & 1;
-            SCLK(tp);
             mbar_wait(plan_full + buf, (g >> 1) & 1);
-            SADD(t_plan, tp);
             const uint32_t cnt = uni(s_cnt[buf]);
             if (cnt == kSentinel) break;
             for (uint32_t r = 0; r < cnt; ++r) {
@@ -504,33 +460,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const Spans sp = row_spans<B, CG, C::GRAN>(mk, p.nchunk, cb);
                 uint32_t bytes = (uint32_t)(CG * C::SLAB);
                 (void)bs;
-                SCLK(te);
                 mbar_wait(empty + stage, phase ^ 1u, 1, (uint32_t)stage | ((uint32_t)row << 8));
-                SADD(t_empty, te);
-                SCLK(tt);
-#ifdef SPAN_TRACE
-                ++n_rows;
-#endif
                 const uint32_t sb = smem0 + (uint32_t)stage * p.stage_bytes;
                 const uint32_t fb = smem_u32(full + stage);
                 s_meta[stage] = make_uint2(sp.w[0], sp.w[1]);  // every lane stores the same words
-                if (SPAN_MODE & 4) bytes = 0;
                 __syncwarp();
                 if (rank == 0) mbar_arrive_expect_tx_e(full + stage, bytes);
-                if (!(SPAN_MODE & 4)) tma_3d_e<CG>(&tm_dy, fb, sb, 0, row * B, n0 / C::ATOM_E);
+                tma_3d_e<CG>(&tm_dy, fb, sb, 0, row * B, n0 / C::ATOM_E);
                 __syncwarp();
-                SADD(t_tma, tt);
                 if (++stage == S) { stage = 0; phase ^= 1u; }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(plan_empty + buf);
         }
         if (lane == 0) {
-            STRACE(2);
-            SSET(8, t_plan);
-            SSET(9, t_empty);
-            SSET(10, t_tma);
-            SSET(11, n_rows);
         }
         if (rank == 0) {  // end of the sequence
             mbar_wait(empty + stage, phase ^ 1u, 2, (uint32_t)stage);
@@ -555,10 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             long long t_full = 0, t_iss = 0;
             (void)t_full; (void)t_iss;
             for (;;) {
-                SCLK(tf);
                 mbar_wait(full + stage, phase, 3, (uint32_t)stage | (nmma_dbg << 8));
-                SADD(t_full, tf);
-                SCLK(ti);
                 const uint2 m = s_meta[stage];
                 if (m.x == kSentinel) break;
                 tc_fence_after();
@@ -568,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
                         const uint32_t wc = c == 0 ? m.x : m.y;
-                        if (!wc || (SPAN_MODE & 1)) continue;
+                        if (!wc) continue;
                         const uint32_t ncol = ((wc >> 16) & 0x7FFFu) * (uint32_t)B;
                         mma_ss<KIND, CG>(tmem + (wc & 0xFFFFu), a_lo0 + so + (uint32_t)k * (C::A_KSTEP >> 4), a_hi,
                                          b_lo0 + so + (uint32_t)c * cbb16 + (uint32_t)k * (C::B_KSTEP >> 4), b_hi,
@@ -579,13 +519,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 mma_commit<CG>(empty + stage);  // frees the stage in both CTAs once these MMAs complete
                 __syncwarp();
-                SADD(t_iss, ti);
                 if (++stage == S) { stage = 0; phase ^= 1u; }
             }
             __syncwarp();
             if (lane == 0) {
-                SSET(12, t_full);
-                SSET(13, t_iss);
             }
             mma_commit<CG>(accfull);
         }
@@ -644,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(empty + stage, phase ^ 1u, 4, (uint32_t)stage);
                     const uint32_t xb = smem0 + (uint32_t)stage * p.stage_bytes + C::SLAB;
                     const int h0 = sp.len[0] / CG, h1 = sp.len[1] / CG;
-                    const int total = (SPAN_MODE & 2) ? 0 : (h0 + h1) * PPB;
+                    const int total = (h0 + h1) * PPB;
                     for (int q = tid; q < total; q += 128) {
                         const int blk = q / PPB, off = q % PPB;
                         const int c = blk >= h0;
@@ -677,7 +614,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------ epilogue
         mbar_wait_sleep(accfull, 0);
         tc_fence_after();
-        if (threadIdx.x == 128) STRACE(3);
         const int ew = warp - 4;
         const uint32_t lb = (uint32_t)(ew * 32) << 16;
         const int64_t n = n0 + ew * 32 + lane;
@@ -710,10 +646,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     }
-    if (threadIdx.x == 128) STRACE(4);
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-    if (threadIdx.x == 0) STRACE(5);
     if (warp == 2) {
         tc_fence_after();
         if constexpr (CG == 2)
@@ -773,7 +707,6 @@ static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms, int want_cg) {
         if (pl.stages >= 3 || maxJ <= 2) break;
         --maxJ;
     }
-    if (const char *e = std::getenv("BSRP_WGRAD_STAGES")) pl.stages = std::min(pl.stages, std::max(2, atoi(e)));  // dev sweeps
     pl.ok = pl.stages >= 2 && pl.cb <= C::MAXCB && pl.nchunk <= 2 && pl.cb <= 32 && nbc <= kColCap;
     pl.smem = (int)(pl.stages * pl.stage_bytes) + kFixedSmem;
     const int64_t ctas_per_split = (N / 128) * pl.nkr;  // CTAs (pairs count twice)
@@ -782,38 +715,12 @@ static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms, int want_cg) {
     return pl;
 }
 
-static int env_cg() {
-    const char *e = std::getenv("BSRP_WGRAD_CG");
-    return e && e[0] == '1' ? 1 : 2;
-}
+// CTA pairs (cta_group::2) whenever N allows them (plan_for falls back to CG = 1).
+constexpr int kWantCG = 2;
 
-#ifdef SPAN_DBGBUF
-struct DbgDump {
-    unsigned *h = nullptr;
-    ~DbgDump() {
-        if (!h || !h[0]) return;
-        fprintf(stderr, "span timeouts: %u\n", h[0]);
-        for (unsigned i = 0; i < std::min(h[0], 64u); ++i)
-            fprintf(stderr, "  cta %u warp %u what %u parity %u info 0x%x\n", h[4 + 4 * i], h[5 + 4 * i] >> 16,
-                    h[5 + 4 * i] & 0xFFFF, h[6 + 4 * i], h[7 + 4 * i]);
-    }
-};
-static DbgDump g_dump;
-static void dbg_setup() {
-    if (g_dump.h) return;
-    cudaHostAlloc(&g_dump.h, 4096, cudaHostAllocMapped);
-    memset(g_dump.h, 0, 4096);
-    unsigned *d = nullptr;
-    cudaHostGetDevicePointer(&d, g_dump.h, 0);
-    cudaMemcpyToSymbol(g_dbg, &d, sizeof(d));
-}
-#endif
 
 template <int KIND, int B, int CG>
 static cudaError_t launch_cg(const Plan &pl, const CUtensorMap &tm_dy, const Params &p, cudaStream_t stream) {
-#ifdef SPAN_DBGBUF
-    dbg_setup();
-#endif
     auto kern = wgrad_span_kernel<KIND, B, CG>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     if (e != cudaSuccess) return e;
@@ -843,7 +750,7 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     int dev = 0, sms = kSplitSMs;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const Plan pl = plan_for<KIND, B>(M, K, N, sms, env_cg());
+    const Plan pl = plan_for<KIND, B>(M, K, N, sms, kWantCG);
     if (!pl.ok) return cudaErrorNotSupported;
     const CUtensorMapDataType dt = KIND == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const CUtensorMapSwizzle sw128 = C::TF32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
@@ -881,11 +788,6 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
 
 }  // namespace span
 
-#ifdef SPAN_TRACE
-extern "C" __attribute__((visibility("default"))) int bsr_dev_span_trace(unsigned long long *host) {
-    return (int)cudaMemcpyFromSymbol(host, span::g_strace, sizeof(span::g_strace));
-}
-#endif
 
 size_t wgrad_span_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
     int ns = 1;

@@ -48,11 +48,16 @@
 namespace bsrp {
 namespace tc {
 
-constexpr int kThreads = 416;  // 13 warps (roles below)
 constexpr int kStages = 24;        // rows whose B blocks may be resident at once
 constexpr int kMaxA = 4;           // TMEM A buffers (rows in flight between the A movers and the MMA warps)
 constexpr int kMaxSA = 8;          // shared-memory A ring stages (dY slabs in flight from HBM)
-constexpr int kIssuers = 2;        // MMA-issuing warps (1 and 2), each owning half of the accumulator columns
+constexpr int kMaxIssuers = 4;     // MMA-issuing warps, each owning a contiguous range of accumulator columns
+// FP32 grade (3xTF32): tcgen05's fp32 accumulation truncates (measured: the
+// rel-F error of bf16-exact products grows linearly with the chain length,
+// 3.9e-5 at 200704 rows), so a split's chain of MMAs into one
+// TMEM accumulator is capped; the split-K reduce then sums the partials with
+// round-to-nearest.  4.1e-6 was measured for 2090-row tf32 chains at keep 1.
+constexpr int kX3ChainRows = 1536;
 constexpr int kSmemBudget = 227 * 1024;
 constexpr int kColCap = 1536;      // stored blocks of one metadata chunk (colidx staged in smem; one run each at most)
 constexpr int kStepCap = 64;       // steps of one metadata chunk
@@ -62,6 +67,7 @@ constexpr int kMaxR = 4;           // block rows per step (b = 16)
 constexpr int kFixedSmem = 1024 + 1024 + kStages * 4 + 2 * (16 * kStepCap + 8 * kStepCap * kMaxR + 4 * kColCap) +
                            4 * (kStepCap * kMaxR + 1) + 2 * kColCap;
 constexpr int kSplitSMs = 148;     // bound on split-K CTAs used to size the workspace (B200: 148 SMs)
+constexpr int kMaxSplits = 4096;   // bound on split-K slices (chain-capped FP32-grade plans)
 constexpr int kEpiBytes = 2 * 32 * 128 * 4;  // epilogue staging (two 32 x 128 fp32 tiles, reuses the B ring)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -181,6 +187,36 @@ __device__ __forceinline__ void tc_mma_ts_run(uint32_t d_tmem, uint32_t a_tmem, 
 #undef BSRP_TS_STEP
 #undef BSRP_TS_ARGS
 
+// FP32 grade (KIND 2): per k step three MMAs with A in TMEM --
+//   [d]  += A_hi . B_hi      [dc] += A_lo . B_hi      [dc] += A_hi . B_lo
+// A_lo sits ACOLS TMEM columns after A_hi; the B_lo copy of the B ring sits
+// `blo` descriptor units (16 bytes) after B.
+#define BSRP_X3_HEAD \
+    "{\n.reg .pred p;\n.reg .b32 ah<8>, al<8>, bl<8>, bm<8>;\n.reg .b64 b<8>, c<8>;\nelect.sync _|p, 0xffffffff;\n"
+#define BSRP_X3_STEP(S)                                                                                          \
+    "add.u32 ah" #S ", %2, " #S "*%7;\nadd.u32 al" #S ", ah" #S ", %9;\nadd.u32 bl" #S ", %3, " #S "*%8;\n"        \
+    "add.u32 bm" #S ", bl" #S ", %6;\nmov.b64 b" #S ", {bl" #S ", %4};\nmov.b64 c" #S ", {bm" #S ", %4};\n"          \
+    "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah" #S "], b" #S ", %5, 1;\n"                                    \
+    "@p tcgen05.mma.cta_group::1.kind::tf32 [%1], [al" #S "], b" #S ", %5, 1;\n"                                    \
+    "@p tcgen05.mma.cta_group::1.kind::tf32 [%1], [ah" #S "], c" #S ", %5, 1;\n"
+#define BSRP_X3_ARGS                                                                                  \
+    ::"r"(d_tmem), "r"(dc_tmem), "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(blo), "n"(AKC), \
+        "n"(BK16), "n"(ACOLS)
+template <int NSTEP, int AKC, int BK16, int ACOLS>
+__device__ __forceinline__ void tc_mma_x3_run(uint32_t d_tmem, uint32_t dc_tmem, uint32_t a_tmem, uint32_t b_lo,
+                                              uint32_t b_hi, uint32_t idesc, uint32_t blo) {
+    if constexpr (NSTEP == 4) {
+        asm volatile(BSRP_X3_HEAD BSRP_X3_STEP(0) BSRP_X3_STEP(1) BSRP_X3_STEP(2) BSRP_X3_STEP(3) "}\n" BSRP_X3_ARGS);
+    } else {
+        static_assert(NSTEP == 8, "k steps per block (b = 32 or 64)");
+        asm volatile(BSRP_X3_HEAD BSRP_X3_STEP(0) BSRP_X3_STEP(1) BSRP_X3_STEP(2) BSRP_X3_STEP(3) BSRP_X3_STEP(4)
+                         BSRP_X3_STEP(5) BSRP_X3_STEP(6) BSRP_X3_STEP(7) "}\n" BSRP_X3_ARGS);
+    }
+}
+#undef BSRP_X3_HEAD
+#undef BSRP_X3_STEP
+#undef BSRP_X3_ARGS
+
 // UMMA shared-memory matrix descriptor (sm_100): start, leading-byte offset
 // (stride between MN atoms for swizzled MN-major), stride-byte offset (between
 // K groups), version 1, swizzle layout type.
@@ -198,7 +234,7 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
 // A K-major (A in TMEM), B MN-major, M = 128, N = n.
 template <int KIND>
 __host__ __device__ __forceinline__ uint32_t instr_desc(uint32_t n) {
-    constexpr uint32_t fmt = KIND == 1 ? 1u : 2u;
+    constexpr uint32_t fmt = KIND == 1 ? 1u : 2u;  // bf16 or tf32 (KIND 0 and 2)
     return (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) | ((n >> 3) << 17) | ((128u >> 4) << 24);
 }
 
@@ -233,14 +269,26 @@ struct Params {
     int chunk_steps;             // steps of one metadata chunk (rowptr + colidx staged in smem)
     int sa;                      // shared-memory A ring stages
     uint32_t a_col0;             // first TMEM column of the A buffers
+    uint32_t corr_col;           // FP32 grade: TMEM column of the correction accumulator (main + corr_col)
     int pdl_trig;                // PDL successor trigger: 0 none, 1 at start, 2 at the epilogue
 };
 
+// KIND: 0 = tf32 (one MMA per k step, operands truncated to tf32 by the tensor
+// core), 1 = bf16, 2 = FP32 grade (3xTF32): every operand x is split into
+// hi = x with the low 13 mantissa bits cleared (exactly a tf32 value) and
+// lo = x - hi (exact in fp32), and
+//   D_main += A_hi . B_hi        D_corr += A_lo . B_hi + A_hi . B_lo
+// (A_lo . B_lo, ~2^-22 relative, is dropped); D = D_main + D_corr with one fp32
+// round-to-nearest add in the epilogue.  The corrections have their own TMEM
+// accumulator so the main chain takes one truncating accumulation per k step,
+// as in the tf32 path, instead of three.
 template <int KIND, int B>
 struct Cfg {
+    static constexpr bool X3 = KIND == 2;
     static constexpr int ES = KIND == 1 ? 2 : 4;
     static constexpr int UK = KIND == 1 ? 16 : 8;           // MMA K per instruction
     static constexpr int A_COLS = B * ES / 4;               // TMEM columns of one block row's slab (32-bit, K packed)
+    static constexpr int A_ROW = X3 ? 2 * A_COLS : A_COLS;  // per block row: hi slab [+ lo slab]
     static constexpr int A_KCOLS = UK * ES / 4;             // TMEM columns per MMA K step (8)
     static constexpr int BW = (B * ES < 128) ? B * ES : 128;  // block row bytes per swizzle atom
     static constexpr int B_ATOMS = B * ES / BW;
@@ -250,61 +298,42 @@ struct Cfg {
     // atomicity (UMMA layout type 1, TMA SWIZZLE_128B_ATOM_32B): 128-byte rows,
     // 32-byte chunks permuted by (row % 4), K groups of 4 rows.  bf16 uses the
     // plain SW32/64/128 layouts with K groups of 8 rows.
-    static constexpr bool TF32 = KIND == 0;
+    static constexpr bool TF32 = KIND != 1;
     static constexpr int KGROUP = TF32 ? 4 : 8;             // K rows per swizzle group
     static constexpr int B_SBO = KGROUP * BW;               // bytes between K groups of B
     static constexpr int B_KSTEP = UK * BW;                 // bytes per MMA K step in B
     static constexpr uint32_t B_LAYOUT = TF32 ? 1u : BW == 128 ? 2u : BW == 64 ? 4u : 6u;  // SW128_32B / SW128 / SW64 / SW32
     static_assert(!TF32 || BW == 128, "tf32 MN-major operands need 128-byte block rows (b >= 32)");
     static constexpr int MAX_RUN = 256 / B;                 // blocks per MMA (N <= 256)
-#ifdef WGRAD_G
-    static constexpr int G = WGRAD_G;  // dev sweeps only
-#else
     static constexpr int G = BLOCK_BYTES >= 8192 ? 1 : BLOCK_BYTES >= 2048 ? 4 : 8;  // blocks per B TMA
-#endif
     // One pipeline step = R consecutive block rows (64 dY rows): one dY slab TMA,
     // one TMEM A buffer, one trip through every barrier.  The per-step
     // synchronisation (each mbarrier wait costs ~100 cycles even when the phase
     // has completed) is paid once per 64 rows instead of once per block row.
-#ifdef WGRAD_R
-    static constexpr int R = WGRAD_R;  // dev sweeps only
-#else
-    static constexpr int R = B >= 64 ? 1 : 64 / B;
-#endif
+    // FP32 grade: one block row per step (its A buffer holds hi and lo).
+    static constexpr int R = (X3 || B >= 64) ? 1 : 64 / B;
     static constexpr int SROWS = R * B;                     // dY rows per step
-    static constexpr int A_STEP = R * A_COLS;               // TMEM columns of one step's A buffer
+    static constexpr int A_STEP = R * A_ROW;                // TMEM columns of one step's A buffer
     static constexpr int SLAB = SROWS * 128 * ES;           // one dY slab (SROWS rows x 128 columns, row-major)
+    static constexpr int ACC_MULT = X3 ? 2 : 1;             // accumulators (main [+ correction])
+    // A single warp issues one tcgen05.mma per ~45-55 cycles (measured,
+    // DESIGN.md §6); the FP32 grade issues 3x the MMAs, from four warps.
+    static constexpr int ISSUERS = X3 ? 4 : 2;
+    static constexpr int SPLITTERS = X3 ? 4 : 0;            // warps splitting landed B blocks into hi / lo
+    // warps: 0 B producer, 1-2 MMA, 3 planner, 4-7 A movers (even steps) + epilogue,
+    // 8 A producer, 9-12 A movers (odd steps), then extra MMA issuers, then splitters
+    static constexpr int WARPS = 13 + (ISSUERS - 2) + SPLITTERS;
+    static constexpr int THREADS = 32 * WARPS;
+    static constexpr int SPLIT_W0 = 13 + (ISSUERS - 2);     // first splitter warp
+    static constexpr int BAR1_THREADS = 32 * (8 + ISSUERS);  // issuers + A movers (accumulator zeroed)
 };
-
-#ifdef WGRAD_TRACE
-__device__ unsigned long long g_trace[160][256];
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define TRACE(slot) (g_trace[blockIdx.x][(slot)] = gtime())
-__device__ long long g_lat[160][4][64];  // [cta][B issue, B ready, A issue, A ready][step j < 64]
-#define TLAT(kind, j) do { if ((j) < 64) g_lat[blockIdx.x][kind][(j)] = clock64(); } while (0)
-#define TCLK(v) const long long v = clock64()
-#define TADD(acc, v) (acc += clock64() - (v))
-#define TSET(slot, val) (g_trace[blockIdx.x][(slot)] = (unsigned long long)(val))
-#else
-#define TRACE(slot) ((void)0)
-#define TCLK(v) ((void)0)
-#define TADD(acc, v) ((void)0)
-#define TSET(slot, val) ((void)0)
-#define TLAT(kind, j) ((void)0)
-#endif
-#ifndef WGRAD_TRACE_MODE
-#define WGRAD_TRACE_MODE 0  // dev experiments only: bit 0 = no MMAs, bit 1 = no B loads, bit 2 = no A loads
-#endif
 
 // This thread's dY column of the step's slab in shared memory (row-major, 128
 // columns per row): SROWS values; consecutive lanes read consecutive elements
 // (conflict-free).
 template <int KIND, int N_>
 __device__ __forceinline__ void lds_slab(uint32_t (&v)[N_], uint32_t saddr) {
+    static_assert(KIND == 0 || KIND == 1, "lds_slab: tf32 / fp32-grade use KIND 0");
 #pragma unroll
     for (int k = 0; k < N_; ++k) {
         if constexpr (KIND == 1) {
@@ -319,6 +348,14 @@ __device__ __forceinline__ void lds_slab(uint32_t (&v)[N_], uint32_t saddr) {
 
 // The slab into TMEM columns [taddr, taddr + N_ * ES / 4) of this thread's lane
 // (K-major A: column j holds K element j, or K elements 2j, 2j+1 for bf16).
+// fp32 -> (hi, lo): hi keeps the sign, exponent and the 10 mantissa bits a tf32
+// operand holds; lo = x - hi is exact in fp32 (and again truncated to tf32 by the
+// tensor core: a 2^-22-relative term).
+__device__ __forceinline__ uint32_t tf32_hi(uint32_t x) { return x & 0xffffe000u; }
+__device__ __forceinline__ uint32_t tf32_lo(uint32_t x) {
+    return __float_as_uint(__uint_as_float(x) - __uint_as_float(x & 0xffffe000u));
+}
+
 template <int KIND, int N_>
 __device__ __forceinline__ void store_slab(uint32_t taddr, const uint32_t (&v)[N_]) {
     if constexpr (KIND == 1) {
@@ -329,6 +366,19 @@ __device__ __forceinline__ void store_slab(uint32_t taddr, const uint32_t (&v)[N
             for (int i = 0; i < 8; ++i) w[i] = v[2 * (c + i)] | (v[2 * (c + i) + 1] << 16);
             tmem_st8(taddr + c, w);
         }
+    } else if constexpr (KIND == 2) {
+        // hi slab at [taddr, taddr + N_), lo slab right after it
+#pragma unroll
+        for (int c = 0; c < N_; c += 8) {
+            uint32_t h[8], l[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                h[i] = tf32_hi(v[c + i]);
+                l[i] = tf32_lo(v[c + i]);
+            }
+            tmem_st8(taddr + c, h);
+            tmem_st8(taddr + N_ + c, l);
+        }
     } else {
 #pragma unroll
         for (int c = 0; c < N_; c += 8) tmem_st8(taddr + c, v + c);
@@ -336,18 +386,20 @@ __device__ __forceinline__ void store_slab(uint32_t taddr, const uint32_t (&v)[N
 }
 
 template <int KIND, int B>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
     wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_val,
                     const __grid_constant__ CUtensorMap tm_dw, const __grid_constant__ CUtensorMap tm_ws, Params p) {
     using C = Cfg<KIND, B>;
     constexpr int R = C::R;
-    // shared memory: [A ring: sa x SLAB][B ring: nbslots x BLOCK_BYTES][slot use: kStages][mbarriers]
-    //   [TMEM slot][step records][sub-row records][run words][rowptr scratch][colidx scratch]
+    // shared memory: [A ring: sa x SLAB][B ring: nbslots x BLOCK_BYTES][FP32 grade: B_lo ring, same
+    //   size][slot use: kStages][mbarriers][TMEM slot][step records][sub-row records][run words]
+    //   [rowptr scratch][colidx scratch]
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *ringA = smem;
     uint8_t *ringB = ringA + (size_t)p.sa * C::SLAB;
-    uint32_t *s_used = reinterpret_cast<uint32_t *>(ringB + (size_t)p.nbslots * C::BLOCK_BYTES);
+    const size_t ringB_bytes = (size_t)p.nbslots * C::BLOCK_BYTES;
+    uint32_t *s_used = reinterpret_cast<uint32_t *>(ringB + ringB_bytes * C::ACC_MULT);
     uint64_t *full = reinterpret_cast<uint64_t *>(s_used + kStages);
     uint64_t *empty = full + kStages;
     uint64_t *afull = empty + kStages;     // [kMaxA]
@@ -357,7 +409,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *accfull = sempty + kMaxSA;
     uint64_t *plan_full = accfull + 1;     // [2]
     uint64_t *plan_empty = plan_full + 2;  // [2]
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(plan_empty + 2);
+    uint64_t *lofull = plan_empty + 2;     // [kStages] FP32 grade: the step's B blocks split into hi / lo
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(lofull + kStages);
     // s_steps [2][kStepCap] (one per step of the chunk): x = MMA runs, y = B-ring
     //   slots used (needs + wasted tail slots) | in-sequence << 30, z = first run
     //   word, w = B bytes
@@ -401,29 +454,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     // their dY slabs are requested before the planner has read rowptr/colidx, so
     // the first HBM round trip overlaps the plan (an empty step costs one slab).
     const int n_spec = (int)min((int64_t)min(p.sa, first_steps), nsteps_cta);
-    // MMA warp 1 owns accumulator blocks [0, jhalf), warp 2 blocks [jhalf, nbJ)
-    const int jhalf = (nbJ + 1) / 2;
-    if (threadIdx.x == 0) TRACE(0);
+    // MMA issuer i owns accumulator blocks [jb(i), jb(i + 1)); runs never cross a boundary
+    auto jb = [&](int i) -> int { return (i * nbJ + C::ISSUERS - 1) / C::ISSUERS; };
+    auto is_boundary = [&](int J) -> bool {
+        bool r = false;
+#pragma unroll
+        for (int i = 1; i < C::ISSUERS; ++i) r |= J == jb(i);
+        return r;
+    };
 
     if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_val)) : "memory");
     if (warp == 8 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_dy)) : "memory");
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(full + s, 1);          // the B producer (+ TMA bytes)
-            mbar_init(empty + s, kIssuers);  // the MMA warps' commits
+            mbar_init(full + s, 1);              // the B producer (+ TMA bytes)
+            mbar_init(empty + s, C::ISSUERS);    // the MMA warps' commits
+            mbar_init(lofull + s, C::SPLITTERS ? C::SPLITTERS : 1);  // one arrival per splitter warp
         }
         for (int a = 0; a < kMaxA; ++a) {
-            mbar_init(afull + a, 4);          // one arrival per A-mover warp
-            mbar_init(aempty + a, kIssuers);  // the MMA warps' commits
+            mbar_init(afull + a, 4);              // one arrival per A-mover warp
+            mbar_init(aempty + a, C::ISSUERS);    // the MMA warps' commits
         }
         for (int s = 0; s < kMaxSA; ++s) {
             mbar_init(sfull + s, 1);   // the A producer's expect_tx (+ TMA bytes)
             mbar_init(sempty + s, 4);  // one arrival per A-mover warp
         }
-        mbar_init(accfull, kIssuers);
+        mbar_init(accfull, C::ISSUERS);
         for (int i = 0; i < 2; ++i) {
             mbar_init(plan_full + i, 1);
-            mbar_init(plan_empty + i, kIssuers);  // the MMA warps release a plan chunk
+            mbar_init(plan_empty + i, C::ISSUERS);  // the MMA warps release a plan chunk
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -493,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         int jprev = -2, rlen = 0;
                         for (int k = 0; k < cnt[q]; ++k) {
                             const int J = (int)s_col[a + k] - J0;
-                            if (J == jprev + 1 && rlen < C::MAX_RUN && J != jhalf) {
+                            if (J == jprev + 1 && rlen < C::MAX_RUN && !is_boundary(J)) {
                                 ++rlen;
                             } else {
                                 ++nruns;
@@ -550,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         };
                         for (int i = 0; i < cnt[q]; ++i) {
                             const int J = (int)s_col[q0[q] + i] - J0;
-                            if (J == jprev + 1 && rlen < C::MAX_RUN && J != jhalf) {
+                            if (J == jprev + 1 && rlen < C::MAX_RUN && !is_boundary(J)) {
                                 ++rlen;
                             } else {
                                 if (rlen) emit();
@@ -569,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // Warm L2 with the chunk's stored blocks (one bulk prefetch per 32 KB, issued by
             // the first n-tile's CTA): the B loads of the 128-column tiles sharing these
             // block rows then hit L2 instead of all waiting on the same HBM fill.
-            if (nt == 0 && !(WGRAD_TRACE_MODE & 8)) {
+            if (nt == 0) {
                 const int64_t b0 = (int64_t)base * C::BLOCK_BYTES, nb = (int64_t)total * C::BLOCK_BYTES;
                 for (int64_t o = (int64_t)lane * 32768; o < nb; o += 32 * 32768) {
                     const uint32_t sz = (uint32_t)min((int64_t)32768, nb - o);
@@ -586,16 +645,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             // 4-D TMA.
             int j = 0;  // steps issued so far
             int tail = 0, bfree = p.nbslots;
-            long long tr_wait = 0, tr_plan = 0, tr_tma = 0;
-            (void)tr_wait; (void)tr_plan; (void)tr_tma;
-            TCLK(tr_start);
             const uint32_t sB0 = smem_u32(ringB);
             for (int c = 0; c < nchunks; ++c) {
                 const int buf = c & 1;
                 const int ns = chunk_len(c);
-                TCLK(tp0);
                 mbar_wait(plan_full + buf, (c >> 1) & 1);
-                TADD(tr_plan, tp0);
                 const int4 *steps = s_steps + buf * kStepCap;
                 const uint2 *subs = s_sub + buf * kStepCap * R;
                 for (int st = 0; st < ns; ++st) {
@@ -607,70 +661,52 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // free slots past the head, or an empty ring (a step that wrapped may
                     // count more than nbslots; bfree then goes negative until it is reclaimed)
                     while (j - tail >= kStages || (bfree < used && bfree < p.nbslots)) {
-                        TCLK(tw0);
                         mbar_wait(empty + tail % kStages, (uint32_t)(tail / kStages) & 1u);
-                        TADD(tr_wait, tw0);
                         bfree += (int)s_used[tail % kStages];
                         ++tail;
                     }
                     s_used[stage] = (uint32_t)used;
                     bfree -= used;
-                    TCLK(tt0);
-                    TLAT(0, j);
-                    if (WGRAD_TRACE_MODE & 2) {
-                        mbar_arrive(full + stage);
-                    } else {
-                        mbar_arrive_expect_tx(full + stage, (uint32_t)rs.w);
+                    mbar_arrive_expect_tx(full + stage, (uint32_t)rs.w);
 #pragma unroll
-                        for (int q = 0; q < R; ++q) {
-                            const uint2 sb = subs[st * R + q];
-                            const int nd = (int)(sb.y >> 16);
-                            const uint32_t dst = sB0 + (sb.y & 0xFFFFu) * C::BLOCK_BYTES;
-                            for (int g = 0; g < nd; g += C::G)
-                                tma_load_4d(&tm_val, full + stage, dst + g * C::BLOCK_BYTES, 0, 0, 0, (int)sb.x + g);
-                        }
+                    for (int q = 0; q < R; ++q) {
+                        const uint2 sb = subs[st * R + q];
+                        const int nd = (int)(sb.y >> 16);
+                        const uint32_t dst = sB0 + (sb.y & 0xFFFFu) * C::BLOCK_BYTES;
+                        for (int g = 0; g < nd; g += C::G)
+                            tma_load_4d(&tm_val, full + stage, dst + g * C::BLOCK_BYTES, 0, 0, 0, (int)sb.x + g);
                     }
-                    TADD(tr_tma, tt0);
                     ++j;
                 }
             }
-            TSET(214, tr_wait);
-            TSET(215, clock64() - tr_start);
-            TSET(216, tr_plan);
-            TSET(217, j);
-            TSET(208, 0);
-            TSET(209, tr_tma);
         }
-    } else if (warp == 1 || warp == 2) {
+    } else if (warp == 1 || warp == 2 || (warp >= 13 && warp < C::SPLIT_W0)) {
         // ------------------------------------------------ MMA issuers (whole warps, one elected lane issues)
-        // Warp 1 issues the runs in accumulator blocks [0, jhalf), warp 2 those in
-        // [jhalf, nbJ): a run's issue cost is a dependent chain (redux -> descriptor
-        // -> uniform registers -> UTCHMMA) of a few hundred cycles, and two warps on
-        // different SM sub-partitions overlap their chains.  Both walk the plan: a
-        // ballot over 32 step records finds the steps in the sequence, lane i loads
-        // run word i of the step with ONE shared load, a ballot selects this warp's
-        // runs and each run word becomes warp-uniform with a single masked redux.
+        // Issuer i (warps 1, 2, then 13.. for the FP32 grade) issues the runs in
+        // accumulator blocks [jb(i), jb(i + 1)): a warp issues one tcgen05.mma per
+        // ~45-55 cycles whatever its shape (measured), so several warps on
+        // different SM sub-partitions keep the tensor pipe fed.  Each walks the
+        // plan: a ballot over 32 step records finds the steps in the sequence,
+        // lane i loads run word i of the step with ONE shared load, a ballot
+        // selects this warp's runs and each run word becomes warp-uniform with a
+        // single masked redux.
         tc_fence_before();
-        asm volatile("bar.sync 1, 320;" ::: "memory");  // accumulator zeroed by warps 4-7
+        asm volatile("bar.sync 1, %0;" ::"r"(C::BAR1_THREADS) : "memory");  // accumulator zeroed by warps 4-7
         tc_fence_after();
-        const bool upper = warp == 2;
-        const uint32_t col_split = (uint32_t)(jhalf * B);
+        const int iw = warp <= 2 ? warp - 1 : warp - 11;
+        const uint32_t col_lo = (uint32_t)(jb(iw) * B), col_hi = (uint32_t)(jb(iw + 1) * B);
         // warp-uniform copies (REDUX results live in uniform registers)
         const uint32_t tmem_u = __reduce_or_sync(0xffffffffu, tmem);
         const uint64_t b_desc0 = smem_desc(smem_u32(ringB), C::B_LBO, C::B_SBO, C::B_LAYOUT);
         const uint32_t b_lo0 = __reduce_or_sync(0xffffffffu, (uint32_t)b_desc0);
         const uint32_t b_hi = __reduce_or_sync(0xffffffffu, (uint32_t)(b_desc0 >> 32));
+        const uint32_t blo_off = __reduce_or_sync(0xffffffffu, (uint32_t)(ringB_bytes >> 4));  // B_lo ring (FP32 grade)
+        const uint32_t corr = __reduce_or_sync(0xffffffffu, p.corr_col);
         const uint32_t idesc0 = instr_desc<KIND>(0u);
         const uint32_t a_tm0 = tmem_u + p.a_col0;
+        uint64_t *ready = C::X3 ? lofull : full;  // FP32 grade: B split into hi / lo by the splitter warps
         int stage = 0, a = 0;
         uint32_t phase = 0, aphase = 0;
-        long long tr_wf = 0, tr_wa = 0, tr_is = 0, tr_loop = 0, tr_nm = 0;
-        (void)tr_wf; (void)tr_wa; (void)tr_is; (void)tr_loop; (void)tr_nm;
-#ifdef WGRAD_TRACE
-        int jm = 0;
-#endif
-        TCLK(tr_start);
-        if (lane == 0 && !upper) TRACE(205);
         for (int c = 0; c < nchunks; ++c) {
             const int buf = c & 1;
             const int ns = chunk_len(c);
@@ -683,28 +719,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int l = __ffs(seq) - 1;
                     const uint32_t nruns = __reduce_or_sync(0xffffffffu, lane == l ? (uint32_t)rec.x : 0u);
                     const uint32_t off = __reduce_or_sync(0xffffffffu, lane == l ? (uint32_t)rec.z : 0u);
-                    TCLK(tw0);
-                    mbar_wait(full + stage, phase);
-                    TADD(tr_wf, tw0);
-#ifdef WGRAD_TRACE
-                    if (!upper && lane == 0) TLAT(1, jm);
-                    ++jm;
-#endif
-                    TCLK(tw1);
+                    mbar_wait(ready + stage, phase);
                     mbar_wait(afull + a, aphase);
-                    TADD(tr_wa, tw1);
-                    TCLK(tw2);
                     tc_fence_after();
                     const uint32_t a_tm = a_tm0 + (uint32_t)(a * C::A_STEP);
-                    TCLK(tw3);
                     for (uint32_t w0 = 0; w0 < nruns; w0 += 32) {
                         const uint32_t wl = w0 + lane < nruns ? runs[off + w0 + lane] : 0u;
-                        uint32_t mine = __ballot_sync(0xffffffffu, w0 + lane < nruns &&
-                                                                       (((wl & 0x3FFu) >= col_split) == upper));
-                        if (WGRAD_TRACE_MODE & 1) mine = 0;
-#ifdef WGRAD_TRACE
-                        tr_nm += __popc(mine);
-#endif
+                        const uint32_t col = wl & 0x3FFu;
+                        uint32_t mine = __ballot_sync(0xffffffffu, w0 + lane < nruns && col >= col_lo && col < col_hi);
                         while (mine) {
                             const int i = __ffs(mine) - 1;
                             mine &= mine - 1;
@@ -712,18 +734,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint32_t d = tmem_u + (rw & 0x3FFu);
                             const uint32_t b_lo = b_lo0 + ((rw >> 10) & 0xFFFu) * (uint32_t)(C::BLOCK_BYTES >> 4);
                             const uint32_t idesc = idesc0 | ((((rw >> 22) & 0x3Fu) * (uint32_t)B >> 3) << 17);
-                            const uint32_t a_q = a_tm + ((rw >> 28) & 0x3u) * (uint32_t)C::A_COLS;
-                            tc_mma_ts_run<KIND, B / C::UK, C::A_KCOLS, (C::B_KSTEP >> 4)>(d, a_q, b_lo, b_hi, idesc);
+                            const uint32_t a_q = a_tm + ((rw >> 28) & 0x3u) * (uint32_t)C::A_ROW;
+                            if constexpr (C::X3)
+                                tc_mma_x3_run<B / C::UK, C::A_KCOLS, (C::B_KSTEP >> 4), C::A_COLS>(d, d + corr, a_q, b_lo, b_hi,
+                                                                                                 idesc, blo_off);
+                            else
+                                tc_mma_ts_run<KIND, B / C::UK, C::A_KCOLS, (C::B_KSTEP >> 4)>(d, a_q, b_lo, b_hi, idesc);
                         }
                     }
-                    TADD(tr_loop, tw3);
                     __syncwarp();
                     if (lane == 0) {
                         tc_commit(empty + stage);  // frees the stage (and its B slots) once these MMAs complete
                         tc_commit(aempty + a);     // frees the A buffer
                     }
                     __syncwarp();
-                    TADD(tr_is, tw2);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                     if (++a == p.na) { a = 0; aphase ^= 1; }
                 }
@@ -731,15 +755,46 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(plan_empty + buf);  // this chunk's plan is no longer read
         }
-        if (lane == 0 && !upper) {
-            TSET(218, tr_wf);
-            TSET(219, tr_wa);
-            TSET(220, clock64() - tr_start);
-            TSET(221, tr_is);
-            TSET(223, tr_loop);
-            TSET(224, tr_nm);
-        }
         if (lane == 0) tc_commit(accfull);
+    } else if (C::X3 && warp >= C::SPLIT_W0) {
+        // ------------------------------------------------ B splitters (FP32 grade)
+        // Walk the B producer's step sequence; once a step's blocks have landed
+        // (`full`), rewrite every value x of its B-ring slots as hi(x) in place and
+        // write lo(x) at the same offset of the B_lo ring (element-wise, so the
+        // swizzled layout and the MMA descriptors carry over), then make the
+        // generic-proxy writes visible to the tensor core and arrive on `lofull`.
+        const int sw = warp - C::SPLIT_W0;
+        int j = 0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int buf = c & 1;
+            const int ns = chunk_len(c);
+            mbar_wait(plan_full + buf, (c >> 1) & 1);
+            const int4 *steps = s_steps + buf * kStepCap;
+            const uint2 *subs = s_sub + buf * kStepCap * R;
+            for (int st = 0; st < ns; ++st) {
+                const int4 rs = steps[st];
+                if (!(rs.y >> 30)) continue;
+                const int stage = j % kStages;
+                mbar_wait(full + stage, (uint32_t)(j / kStages) & 1u);
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const uint2 sb = subs[st * R + q];
+                    const int nd = (int)(sb.y >> 16);
+                    uint4 *hi = reinterpret_cast<uint4 *>(ringB + (size_t)(sb.y & 0xFFFFu) * C::BLOCK_BYTES);
+                    uint4 *lo = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(hi) + ringB_bytes);
+                    const int n16 = nd * (C::BLOCK_BYTES / 16);
+                    for (int i = sw * 32 + lane; i < n16; i += 32 * C::SPLITTERS) {
+                        const uint4 x = hi[i];
+                        hi[i] = make_uint4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+                        lo[i] = make_uint4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(lofull + stage);
+                ++j;
+            }
+        }
     } else if (warp >= 4) {
         // ------------------------------------------------ A producer (warp 8) and A movers (warps 4-7, 9-12)
         // Step j of the sequence: warp 8 lane 0 requests its dY slab (one 2-D TMA,
@@ -772,31 +827,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         const uint32_t sA0 = smem_u32(ringA);
         if (warp == 8) {
-            long long tr_w = 0;
-            (void)tr_w;
             int64_t S;
             for (int j = 0; next_step(S); ++j) {
                 if (lane == 0) {
                     const int s = j % p.sa;
-                    TCLK(tw0);
                     if (j >= p.sa) mbar_wait(sempty + s, (uint32_t)((j / p.sa) - 1) & 1u);
-                    TADD(tr_w, tw0);
-                    TLAT(2, j);
-                    if (WGRAD_TRACE_MODE & 4) {
-                        mbar_arrive(sfull + s);
-                    } else {
-                        mbar_arrive_expect_tx(sfull + s, (uint32_t)C::SLAB);
-                        asm volatile(
-                            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-                                sA0 + (uint32_t)(s * C::SLAB)),
-                            "l"(reinterpret_cast<uint64_t>(&tm_dy)), "r"(n0), "r"((int)(S * C::SROWS)),
-                            "r"(smem_u32(sfull + s))
-                            : "memory");
-                    }
+                    mbar_arrive_expect_tx(sfull + s, (uint32_t)C::SLAB);
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                            sA0 + (uint32_t)(s * C::SLAB)),
+                        "l"(reinterpret_cast<uint64_t>(&tm_dy)), "r"(n0), "r"((int)(S * C::SROWS)),
+                        "r"(smem_u32(sfull + s))
+                        : "memory");
                 }
                 __syncwarp();
             }
-            if (lane == 0) TSET(206, tr_w);
         } else {
             const int ew = warp & 3;
             const int par = warp >= 9;
@@ -804,51 +849,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             // zero the accumulator columns this CTA owns (MMAs then always accumulate)
             if (!par) {
                 for (int c = 0; c < nbJ * B; c += 16) tmem_st16_zero(tmem + lane_base + c);
+                if constexpr (C::X3)
+                    for (int c = 0; c < nbJ * B; c += 16) tmem_st16_zero(tmem + lane_base + p.corr_col + c);
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
             tc_fence_before();
-            asm volatile("bar.sync 1, 320;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"r"(C::BAR1_THREADS) : "memory");
             tc_fence_after();
             const uint32_t a_tm0 = tmem + lane_base + p.a_col0;
             const uint32_t my_col = (uint32_t)((ew * 32 + lane) * C::ES);
-            long long tr_wa = 0, tr_st = 0, tr_ld = 0, tr_sw = 0;
-            (void)tr_wa; (void)tr_st; (void)tr_ld; (void)tr_sw;
-            TCLK(tr_start);
             int j = 0;
             int64_t S;
             for (; next_step(S); ++j) {
                 if ((j & 1) != par) continue;
-                TCLK(tl0);
                 const int s = j % p.sa;
-                TCLK(tsw);
                 mbar_wait(sfull + s, (uint32_t)(j / p.sa) & 1u);
-                TADD(tr_sw, tsw);
-                if (lane == 0 && ew == 0) TLAT(3, j);
                 uint32_t v[C::SROWS];
-                lds_slab<KIND, C::SROWS>(v, sA0 + (uint32_t)(s * C::SLAB) + my_col);
+                lds_slab<(KIND == 1 ? 1 : 0), C::SROWS>(v, sA0 + (uint32_t)(s * C::SLAB) + my_col);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(sempty + s);
-                TADD(tr_ld, tl0);
                 const int ab = j % p.na;
-                TCLK(tw0);
                 if (j >= p.na) mbar_wait(aempty + ab, (uint32_t)((j / p.na) - 1) & 1u);
-                TADD(tr_wa, tw0);
-                TCLK(ts0);
                 tc_fence_after();
-                store_slab<KIND, C::SROWS>(a_tm0 + (uint32_t)(ab * C::A_STEP), v);
+                if constexpr (C::X3) store_slab<2, C::SROWS>(a_tm0 + (uint32_t)(ab * C::A_STEP), v);
+                else store_slab<KIND, C::SROWS>(a_tm0 + (uint32_t)(ab * C::A_STEP), v);
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                TADD(tr_st, ts0);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(afull + ab);
-            }
-            if (threadIdx.x == 128) {
-                TSET(210, tr_wa);
-                TSET(211, clock64() - tr_start);
-                TSET(212, j);
-                TSET(213, tr_st);
-                TSET(222, tr_ld);
-                TSET(207, tr_sw);
             }
         }
     }
@@ -863,7 +891,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait_sleep(accfull, 0);
         if (p.pdl_trig == 2) pdl_trigger();
         tc_fence_after();
-        if (threadIdx.x == 128) TRACE(203);
         const int ew = warp - 4;
         const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
         float *stage_buf = reinterpret_cast<float *>(ringA);  // 2 x [32][128] over the idle A/B rings
@@ -879,7 +906,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t v[32];
             TMEM_LD16(tmem + lane_base + c, v);
             TMEM_LD16(tmem + lane_base + c + 16, (v + 16));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if constexpr (C::X3) {  // D = D_main + D_corr, one round-to-nearest fp32 add
+                uint32_t w[32];
+                TMEM_LD16(tmem + lane_base + p.corr_col + c, w);
+                TMEM_LD16(tmem + lane_base + p.corr_col + c + 16, (w + 16));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__fadd_rn(__uint_as_float(v[i]), __uint_as_float(w[i])));
+            } else {
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            }
 #pragma unroll
             for (int i = 0; i < 32; ++i) sb[i * 128 + ew * 32 + lane] = __uint_as_float(v[i]);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -905,7 +941,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (threadIdx.x == 128) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
-    if (threadIdx.x == 128) TRACE(204);
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
@@ -972,7 +1007,7 @@ static cudaError_t make_map(CUtensorMap *tm, const void *base, CUtensorMapDataTy
 
 struct Plan {
     int kr_blocks, nkr, nbslots, na, sa, nsplit, smem, chunk_steps;
-    uint32_t a_col0;
+    uint32_t a_col0, corr_col;
 };
 
 // sms: SMs the split-K grid may fill (the device's count at launch, kSplitSMs
@@ -986,28 +1021,32 @@ static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms) {
     // goes to the B ring (measured: with fp32 blocks the B ring's depth, not the A
     // ring's, bounds the main loop)
     pl.sa = std::max(2, std::min(kMaxSA, 65536 / C::SLAB));
-#ifdef WGRAD_SA
-    pl.sa = WGRAD_SA;  // dev sweeps only
-#endif
-    const int ring = kSmemBudget - kFixedSmem - pl.sa * C::SLAB;
-    // largest kcol range whose accumulator leaves room for two A buffers in the
+    // B ring (FP32 grade: plus its B_lo copy of the same size)
+    const int ring = (kSmemBudget - kFixedSmem - pl.sa * C::SLAB) / C::ACC_MULT;
+    // largest kcol range whose accumulator(s) leave room for two A buffers in the
     // 512 TMEM columns and whose densest step (R block rows, every block, G rounded)
     // fits the B ring; <= 56 blocks keeps a run word's column in 10 bits
-    int maxb = std::min(std::min((512 - 2 * C::A_STEP) / B, 56), nbc);
+    int maxb = std::min(std::min((512 - 2 * C::A_STEP) / (B * C::ACC_MULT), 56), nbc);
     auto need_of = [](int blocks) { return (blocks + C::G - 1) / C::G * C::G; };
     while (maxb > 1 && C::R * need_of(maxb) * C::BLOCK_BYTES > ring) --maxb;
     pl.nkr = (nbc + maxb - 1) / maxb;
     pl.kr_blocks = (nbc + pl.nkr - 1) / pl.nkr;
-    pl.na = std::min(kMaxA, (512 - pl.kr_blocks * B) / C::A_STEP);
+    pl.corr_col = (uint32_t)(pl.kr_blocks * B);
+    pl.na = std::min(kMaxA, (512 - C::ACC_MULT * pl.kr_blocks * B) / C::A_STEP);
     pl.a_col0 = (uint32_t)(512 - pl.na * C::A_STEP);
     pl.nbslots = std::min(4095, ring / C::BLOCK_BYTES);
-    pl.smem = pl.sa * C::SLAB + pl.nbslots * C::BLOCK_BYTES + kFixedSmem;
+    pl.smem = pl.sa * C::SLAB + C::ACC_MULT * pl.nbslots * C::BLOCK_BYTES + kFixedSmem;
     // a chunk's stored blocks (all columns) fit the colidx / run-word buffers
     pl.chunk_steps = std::min(kStepCap, kColCap / (C::R * nbc));
     const int64_t tiles = (N / 128) * pl.nkr;
     const int64_t nst = (M / B + C::R - 1) / C::R;
     const int64_t cap = std::min<int64_t>(sms, kSplitSMs);
-    pl.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nst, cap / std::max<int64_t>(1, tiles)));
+    int64_t ns = std::max<int64_t>(1, cap / std::max<int64_t>(1, tiles));
+    if (C::X3) {  // chain cap: at most kX3ChainRows rows of MMAs per TMEM accumulator
+        const int64_t steps_cap = std::max<int64_t>(1, kX3ChainRows / C::SROWS);
+        ns = std::max<int64_t>(ns, (nst + steps_cap - 1) / steps_cap);
+    }
+    pl.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>({nst, ns, (int64_t)kMaxSplits}));
     return pl;
 }
 
@@ -1065,6 +1104,7 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     p.na = pl.na;
     p.sa = pl.sa;
     p.a_col0 = pl.a_col0;
+    p.corr_col = pl.corr_col;
     p.chunk_steps = pl.chunk_steps;
     p.ws = ws;
     p.mode = pl.nsplit > 1 ? 3 : accumulate ? 1 : 0;
@@ -1073,7 +1113,7 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((N / 128) * pl.nkr * pl.nsplit);
-    e = launch_pdl(pdl_flags() & 16, kern, dim3(grid), dim3(kThreads), (size_t)pl.smem, stream, tm_dy, tm_val, tm_dw, tm_ws, p);
+    e = launch_pdl(pdl_flags() & 16, kern, dim3(grid), dim3(C::THREADS), (size_t)pl.smem, stream, tm_dy, tm_val, tm_dw, tm_ws, p);
     if (e != cudaSuccess) return e;
     count_launch();
     e = cudaGetLastError();
@@ -1119,24 +1159,47 @@ size_t wgrad_tc_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
     return std::max(wgrad_runs_ws_bytes(M, K, b, N), wgrad_span_ws_bytes(M, K, b, N));
 }
 
+// FP32 grade: the chain cap (kX3ChainRows) sets a floor on the splits.  The
+// plan's split count does not depend on the device's SM count beyond 148.
+size_t wgrad_x3_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
+    tc::Plan pl{};
+    if (b == 32) pl = tc::plan_for<2, 32>(M, K, N, tc::kSplitSMs);
+    else if (b == 64) pl = tc::plan_for<2, 64>(M, K, N, tc::kSplitSMs);
+    else return 0;
+    return pl.nsplit > 1 ? (size_t)pl.nsplit * K * N * sizeof(float) : 0;
+}
+
 // Kernel choice (measured): the per-run kernel, except with many
 // block columns (K / b >= 64: S12 fc2 at b = 16, B24 fc2 at b = 32), where it
 // splits the kcols into several TMEM ranges that each re-read dY and issues one
 // MMA per short run, while the span kernel's CTA pairs and dense-padded
 // N <= 256 MMAs win (S12 fc2 bf16 b=16: 124 vs 200 us; B24 fc2 b=32: 2.38 vs
-// 3.92 ms f32/tf32, 1.45 vs 2.91 ms bf16).  BSRP_WGRAD=runs|span forces one.
-static bool use_runs_kernel(int kind, int b, int64_t K) {
+// 3.92 ms f32/tf32, 1.45 vs 2.91 ms bf16).  The FP32 grade exists in the per-run
+// kernel only.
+static bool use_runs_kernel(int kind, int algo, int b, int64_t K) {
+    if (kind == 2) return true;
+    if (algo == 1) return true;
+    if (algo == 2) return false;
     if (kind == 0 && b == 16) return false;  // tf32 b = 16: only the span kernel pairs blocks into 128-byte rows
-    const char *e = std::getenv("BSRP_WGRAD");
-    if (e && std::string(e) == "span") return false;
-    if (e && std::string(e) == "runs") return true;
     return K / b < 64;
 }
 
+bool wgrad_tc_supported(int kind, int algo, int b, int64_t K, int64_t N) {
+    if (N % 128 != 0 || b < 16 || b > 64) return false;
+    if (kind == 2) {
+        if (algo != 0 && algo != 1) return false;
+        if (b == 32) return tc::plan_for<2, 32>(128, K, N, tc::kSplitSMs).chunk_steps >= 1;
+        if (b == 64) return tc::plan_for<2, 64>(128, K, N, tc::kSplitSMs).chunk_steps >= 1;
+        return false;
+    }
+    if (use_runs_kernel(kind, algo, b, K)) return !(kind == 0 && b == 16);
+    return true;
+}
+
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
-                            int kind, int64_t M, int64_t K, int b, const void *dY, int64_t N, float *dW,
+                            int kind, int algo, int64_t M, int64_t K, int b, const void *dY, int64_t N, float *dW,
                             int accumulate, void *ws, cudaStream_t stream) {
-    if (!use_runs_kernel(kind, b, K))
+    if (!use_runs_kernel(kind, algo, b, K))
         return launch_wgrad_span(rowptr, colidx, values, nnzb, kind, M, K, b, dY, N, dW, accumulate, ws, stream);
     if (!values || nnzb == 0) {  // no stored block: dW = 0 (or unchanged)
         return accumulate ? cudaSuccess : cudaMemsetAsync(dW, 0, (size_t)K * N * sizeof(float), stream);
@@ -1144,7 +1207,7 @@ cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const 
 #define TC_CASE(KD, B_) \
     if (kind == KD && b == B_) return tc::launch_t<KD, B_>(rowptr, colidx, values, nnzb, M, K, dY, N, dW, accumulate, \
                                                             static_cast<float *>(ws), stream);
-    TC_CASE(0, 32) TC_CASE(0, 64) TC_CASE(1, 16) TC_CASE(1, 32) TC_CASE(1, 64)
+    TC_CASE(0, 32) TC_CASE(0, 64) TC_CASE(1, 16) TC_CASE(1, 32) TC_CASE(1, 64) TC_CASE(2, 32) TC_CASE(2, 64)
 #undef TC_CASE
     return cudaErrorInvalidValue;
 }

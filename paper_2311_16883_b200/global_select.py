@@ -86,7 +86,7 @@ def prune_global(X, b: int, keep: float, group=None, stream=None):
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     cpu_coll = world > 1 and dist.get_backend(group) == "gloo"
     ws_bytes = lib.bsr_prune_workspace_bytes(M, K, b)
-    ws = workspace(ws_bytes, dev, kind="prune")
+    ws = workspace(ws_bytes, dev, kind="prune", stream=stream)
     st = _stream(stream)
 
     def coll_tensor(a: np.ndarray):

@@ -43,7 +43,7 @@ def prune_rows(X: torch.Tensor, b: int, keep: float, sample_rows: int = 196, str
     out = RowBSR(rowptr=torch.empty(M + 1, dtype=torch.int32, device=X.device),
                  colidx=torch.empty(k, dtype=torch.int32, device=X.device),
                  values=torch.empty((k, b), dtype=X.dtype, device=X.device), M=M, K=K, b=b, sample_rows=sample_rows)
-    ws = workspace(lib.bsr_prune_rows_workspace_bytes(M, K, b), X.device, kind="rows")
+    ws = workspace(lib.bsr_prune_rows_workspace_bytes(M, K, b), X.device, kind="rows", stream=stream)
     _lib.check(lib.bsr_prune_rows(X.data_ptr(), M, K, b, sample_rows, float(keep), _dt(X), out.rowptr.data_ptr(),
                                   out.colidx.data_ptr() if k else None, out.values.data_ptr() if k else None,
                                   ws.data_ptr(), ws.numel(), _stream(stream)))
@@ -70,7 +70,7 @@ def wgrad_rows(A: RowBSR, dY: torch.Tensor, out: torch.Tensor | None = None, acc
     if out is None:
         out = torch.empty(A.K, N, dtype=torch.float32, device=dY.device)
     ws_bytes = lib.bsr_wgrad_rows_workspace_bytes(A.M, A.K, A.b, N)
-    ws = workspace(ws_bytes, dY.device) if ws_bytes else None
+    ws = workspace(ws_bytes, dY.device, stream=stream) if ws_bytes else None
     _lib.check(lib.bsr_wgrad_rows(A.rowptr.data_ptr(), A.colidx.data_ptr() if A.nnz else None,
                                   A.values.data_ptr() if A.nnz else None, A.nnz, A.M, A.K, A.b, _dt(A.values),
                                   dY.data_ptr(), _dt(dY), N, out.data_ptr(), int(accumulate),

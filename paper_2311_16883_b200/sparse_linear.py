@@ -58,11 +58,14 @@ class _SparseLinearFn(torch.autograd.Function):
 
 
 def _default_prec(dtype: torch.dtype, block: int, out_features: int) -> str:
-    if out_features % 128:
-        return "fp32"  # the tensor-core paths need N % 128 == 0
-    if dtype == torch.bfloat16:
+    """dW arithmetic matching what nn.Linear would give: fp32 activations get the
+    FP32-grade path (rel-F <= 1e-5: 3xTF32 tensor cores where the library has them,
+    FFMA otherwise -- the library picks), bf16 activations the bf16 tensor-core
+    path where it exists (b >= 16, N % 128 == 0) and the FP32 FFMA path (which
+    reads bf16 storage) elsewhere."""
+    if dtype == torch.bfloat16 and block >= 16 and out_features % 128 == 0:
         return "bf16"
-    return "tf32" if block >= 16 else "fp32"  # b = 16: tf32 blocks paired per swizzle row (span kernel)
+    return "fp32"
 
 
 def sparse_linear(x: torch.Tensor, weight: torch.Tensor, bias=None, sparsity: float = 0.5, block: int = 16,

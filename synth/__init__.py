@@ -75,6 +75,24 @@ def ints(M: int, K: int, seed: int, lo: int = -2, hi: int = 2) -> np.ndarray:
     return _rng(seed).integers(lo, hi + 1, size=(M, K)).astype(np.float32)
 
 
+def block_count_ints(M: int, K: int, b: int, counts, seed: int) -> np.ndarray:
+    """Tie family at full size: every b x b block holds exactly c entries of +-1
+    (the rest 0), c drawn uniformly from `counts`, so every block's sum of squares
+    is the integer c -- exact in fp32 and in fp64, with few distinct values, i.e.
+    thousands of blocks tied on each value."""
+    rng = _rng(seed)
+    nbr, nbc = M // b, K // b
+    c = rng.choice(np.asarray(counts), size=(nbr, nbc))
+    r = rng.random((nbr, nbc, b * b))
+    order = np.argsort(r, axis=2)  # a random permutation of the block's slots
+    slots = np.arange(b * b)[None, None, :]
+    sel = np.zeros((nbr, nbc, b * b), dtype=bool)
+    np.put_along_axis(sel, order, slots < c[..., None], axis=2)
+    sign = np.where(rng.random((nbr, nbc, b * b)) < 0.5, -1.0, 1.0).astype(np.float32)
+    blk = (sel * sign).reshape(nbr, nbc, b, b).astype(np.float32)
+    return np.ascontiguousarray(blk.transpose(0, 2, 1, 3).reshape(M, K))
+
+
 def to_bf16_bits(x: np.ndarray) -> np.ndarray:
     """fp32 -> bfloat16 bit patterns (uint16), round-to-nearest-even (data prep)."""
     u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)

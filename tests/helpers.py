@@ -43,6 +43,25 @@ def gap_ok(X: np.ndarray, b: int, k: int, rel: float = 1e-5) -> bool:
     return s[k - 1] >= s[k] * (1.0 + rel)
 
 
+def gap_k(X: np.ndarray, b: int, k: int, rel: float = 2e-4) -> int:
+    """The kept count nearest to k whose boundary has a natural relative gap
+    >= rel between the k-th and (k+1)-th largest fp64 block sums of squares, so
+    that the fp32 sums of the GPU select the same set as the oracle's fp64 ones
+    without rescaling X (used for bf16 inputs, where rescaling would leave the
+    bf16 grid).  X: fp32 array or bf16 bit patterns (uint16)."""
+    if X.dtype == np.uint16:
+        X = synth.bf16_bits_to_f32(X)
+    s = np.sort(oracle.block_sumsq(X, b))[::-1]
+    N = s.size
+    if k <= 0 or k >= N:
+        return k
+    for d in range(N):
+        for kk in (k - d, k + d):
+            if 0 < kk < N and s[kk - 1] > s[kk] * (1.0 + rel):
+                return kk
+    return k
+
+
 def make_x(family: str, M: int, K: int, seed: int, b: int, k: int, gap: bool = True) -> np.ndarray:
     X = synth.activation(family, M, K, seed)
     if gap:

@@ -311,6 +311,24 @@ def test_wgrad_bf16_operands():
     np.testing.assert_allclose(dW, ref, rtol=1e-12, atol=1e-15)
 
 
+@pytest.mark.parametrize("bf16", [False, True])
+@pytest.mark.parametrize("keep", [0.0, 0.3, 1.0])
+def test_wgrad_masked_equals_quadruple_loop(bf16, keep):
+    """wgrad_masked (decompress + one BLAS matmul) is the same definition as the
+    quadruple loop: equal to ~1e-12 relative on every keep, f32 and bf16 operands."""
+    M, K, Nout, b = 128, 96, 40, 16
+    X = synth.f_gelu(M, K, seed=13)
+    dY = synth.grad_out(M, Nout, seed=13)
+    if bf16:
+        X, dY = synth.to_bf16_bits(X), synth.to_bf16_bits(dY)
+    out = oracle.prune(X, b, oracle.keep_count(oracle.num_blocks(M, K, b), keep))
+    args = (out["rowptr"], out["colidx"], out["values"], M, K, b, dY)
+    loop = oracle.wgrad(*args)
+    np.testing.assert_allclose(oracle.wgrad_masked(*args), loop, rtol=1e-12, atol=1e-15)
+    if keep == 0.0:
+        assert not oracle.wgrad_masked(*args).any()
+
+
 def test_rel_frobenius():
     B = np.array([[3.0, 4.0]])
     assert oracle.rel_frobenius(B, B) == 0.0

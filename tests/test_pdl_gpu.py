@@ -1,10 +1,10 @@
-"""Programmatic dependent launch (PDL, csrc/launch.h): the BSRP_PDL bit mask only
+"""Programmatic dependent launch (PDL, csrc/launch.h): the bsr_set_pdl bit mask only
 changes WHEN the wgrad / split-K reduce / decompress CTAs are scheduled, never
 what they compute.  Every kernel waits (griddepcontrol.wait) for its stream
 predecessor before its first global access, so prune -> wgrad -> decompress
 chained back to back must give bit-identical BSR, dW and decompressed X under
-every mask, captured in a CUDA graph or launched eagerly.  The mask is read once
-per process, so each mask runs in its own subprocess."""
+every mask, captured in a CUDA graph or launched eagerly.  Each mask runs in its
+own subprocess (fresh graph, fresh workspaces)."""
 import os
 import subprocess
 import sys
@@ -25,6 +25,7 @@ import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 import paper_2311_16883_b200 as bp, synth
 out, M, K, N, b, dt, prec, graph = sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]), int(sys.argv[6]), sys.argv[7], sys.argv[8], sys.argv[9] == "1"
+bp.set_pdl(int(sys.argv[10]))
 tdt = torch.bfloat16 if dt == "bf16" else torch.float32
 X = torch.from_numpy(synth.f_aff(M, K, 4242)).to("cuda", tdt)
 dY = torch.from_numpy(synth.f_aff(M, N, 4343)).to("cuda", tdt)
@@ -59,14 +60,13 @@ np.savez(out, rowptr=A.rowptr.cpu().numpy(), colidx=A.colidx.cpu().numpy(), valu
 
 def _run(tmp_path, mask, args):
     f = tmp_path / f"pdl_{mask}.npz"
-    env = dict(os.environ, BSRP_PDL=str(mask))
-    r = subprocess.run([sys.executable, "-c", _SCRIPT, ROOT, str(f), *map(str, args)], env=env, cwd=ROOT,
+    r = subprocess.run([sys.executable, "-c", _SCRIPT, ROOT, str(f), *map(str, args), str(mask)], cwd=ROOT,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     return np.load(f)
 
 
-@pytest.mark.parametrize("dt,prec", [("f32", "tf32"), ("bf16", "bf16")])
+@pytest.mark.parametrize("dt,prec", [("f32", "tf32"), ("bf16", "bf16"), ("f32", "fp32")])
 @pytest.mark.parametrize("graph", [0, 1])
 def test_pdl_masks_bit_identical(tmp_path, dt, prec, graph):
     # C2-like shape with split-K (reduce kernel in the chain): 6272 x 384 -> 1536, b = 32

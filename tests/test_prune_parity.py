@@ -21,15 +21,6 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_2311_16883_b200 as bp  # noqa: E402
 
 
-@pytest.fixture(autouse=True, params=["small", "multi"])
-def prune_path(request, monkeypatch):
-    """Every case runs on both prune kernels: the one-barrier small-N kernel (every
-    CTA repeats the select over all keys in shared memory, N <= 40960) and the
-    multi-barrier kernel with global histograms (BSRP_PRUNE_SMALL=0)."""
-    monkeypatch.setenv("BSRP_PRUNE_SMALL", "1" if request.param == "small" else "0")
-    return request.param
-
-
 def run_and_compare(Xn: np.ndarray, b: int, k: int, bf16: bool = False):
     """Xn: float32 matrix or uint16 bf16 bit patterns."""
     M, K = Xn.shape

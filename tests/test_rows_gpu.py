@@ -119,3 +119,20 @@ def test_rows_selection_full_s12_batch():
     np.testing.assert_array_equal(A.rowptr.cpu().numpy(), ref["rowptr"])
     np.testing.assert_array_equal(A.colidx.cpu().numpy(), ref["colidx"])
     np.testing.assert_array_equal(A.values.cpu().numpy().view(np.int32), ref["values"].reshape(-1, b).view(np.int32))
+
+
+@pytest.mark.parametrize("S,K,b", [(128, 384, 4), (128, 768, 8)])
+def test_rows_select_keys_at_shared_memory_limit(S, K, b):
+    """A sample of exactly 12288 segment keys (48 KB, the on-chip threshold): the
+    select kernel's dynamic shared memory plus its static arrays exceed the
+    default 48 KB limit, so the launch must opt in."""
+    assert S * K // b == 12288
+    M = 2 * S
+    X = synth.ints(M, K, 77)  # exact sums; ties decided by the flat-index rule
+    ks = oracle.keep_count(S * K // b, 0.5)
+    ref = oracle.prune_per_sample(X, b, ks, S)
+    A = bp.prune_rows(to_torch(X), b, 0.5, sample_rows=S)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(A.rowptr.cpu().numpy(), ref["rowptr"])
+    np.testing.assert_array_equal(A.colidx.cpu().numpy(), ref["colidx"])
+    np.testing.assert_array_equal(A.values.cpu().numpy().view(np.int32), ref["values"].reshape(-1, b).view(np.int32))

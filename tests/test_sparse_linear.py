@@ -91,3 +91,30 @@ def test_saved_activation_is_the_bsr():
     # the caching allocator rounds blocks > 1 MiB to 2 MiB and keeps small pools: allow 1 MiB of slack
     assert held <= bsr_bytes + (1 << 20), (held, bsr_bytes)
     assert held < 0.5 * M * K * 4
+
+
+@pytest.mark.parametrize("block", [4, 8])
+def test_bf16_small_blocks_use_fp32_path(block):
+    """bf16 activations with b < 16 (no tensor-core dW at that block size): the
+    layer's default precision must be the FP32 FFMA path, not bf16."""
+    layer, x, y, x_np, dy_np = run(None, 0.5, block, N=256, dtype=torch.bfloat16)
+    assert layer.weight.grad is not None and torch.isfinite(layer.weight.grad).all()
+    xb, dyb = synth.to_bf16_bits(x_np), synth.to_bf16_bits(dy_np)
+    M, K = x_np.shape
+    k = oracle.keep_count(oracle.num_blocks(M, K, block), 0.5)
+    ref = oracle.prune(xb, block, k)
+    dw_ref = oracle.wgrad(ref["rowptr"], ref["colidx"], ref["values"], M, K, block, dyb)
+    got = layer.weight.grad.detach().float().t().cpu().numpy()
+    assert oracle.rel_frobenius(got, dw_ref) <= 5e-3  # bf16 weight.grad rounding included
+
+
+def test_fp32_layer_defaults_to_fp32_grade():
+    """fp32 activations: the default dW is the FP32 grade (<= 1e-5), as nn.Linear's
+    fp32 weight gradient would be -- not a silent tf32 downgrade."""
+    layer, x, y, x_np, dy_np = run(None, 0.5, 32)
+    M, K = x_np.shape
+    k = oracle.keep_count(oracle.num_blocks(M, K, 32), 0.5)
+    ref = oracle.prune(x_np, 32, k)
+    dw_ref = oracle.wgrad(ref["rowptr"], ref["colidx"], ref["values"], M, K, 32, dy_np)
+    got = layer.weight.grad.detach().t().cpu().numpy()
+    assert oracle.rel_frobenius(got, dw_ref) <= 1e-5
