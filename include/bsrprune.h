@@ -237,6 +237,42 @@ BSR_API bsr_status_t bsr_prune_threshold(const void *X, int64_t M, int64_t K, in
                                          void *ws, size_t ws_bytes, void *stream);
 
 
+/* The same protocol with its state in DEVICE memory, so that no step needs a
+ * device->host copy: the caller's collectives (NCCL on device buffers) run
+ * between stream-ordered calls, and only the final kept count of this rank is
+ * read back (to size the result).  The collective sequence is fixed: three
+ * histogram all-reduces (a resolved level contributes zeros) and one all-gather.
+ *   bsr_gselect_state_bytes   bytes of the opaque state (device, caller-owned).
+ *   bsr_gselect_init          state <- k_total (the kept count of the whole batch).
+ *   bsr_gselect_hist          level 0..2: this rank's digit histogram of the keys
+ *                             matching the state's prefix (level 0 also computes the
+ *                             block sums into ws, as bsr_select_hist); hist uint32
+ *                             [4096 / 1024 / 512], zeroed by the call.
+ *   bsr_gselect_update        after the all-reduce of hist: the boundary bin of the
+ *                             summed histogram joins the prefix (1-CTA kernel).
+ *   bsr_gselect_counts        this rank's (#keys > T, #keys == T): uint64[2].
+ *   bsr_gselect_take          after the all-gather of every rank's counts
+ *                             (uint64 [world][2], rank order): this rank's tie quota
+ *                             and kept count k_rank (state word 7, uint64).
+ *   bsr_prune_gselect         pack with the state's threshold into `out`, whose
+ *                             arrays hold `capacity` >= k_rank blocks (e.g.
+ *                             min(N_rank, k_total)); rowptr[M/b] = k_rank; out->nnzb
+ *                             is set to capacity (the host learns k_rank from state
+ *                             word 7).  With one rank: bit-identical to bsr_prune_k. */
+BSR_API size_t bsr_gselect_state_bytes(void);
+BSR_API bsr_status_t bsr_gselect_init(int64_t k_total, uint64_t *state, void *stream);
+BSR_API bsr_status_t bsr_gselect_hist(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype, int32_t level,
+                                      const uint64_t *state, uint32_t *hist, void *ws, size_t ws_bytes, void *stream);
+BSR_API bsr_status_t bsr_gselect_update(const uint32_t *hist_total, int32_t level, uint64_t *state, void *stream);
+BSR_API bsr_status_t bsr_gselect_counts(int64_t M, int64_t K, int32_t b, const uint64_t *state, uint64_t *counts,
+                                        void *ws, size_t ws_bytes, void *stream);
+BSR_API bsr_status_t bsr_gselect_take(const uint64_t *all_counts, int32_t world, int32_t rank, uint64_t *state,
+                                      void *stream);
+BSR_API bsr_status_t bsr_prune_gselect(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype,
+                                       const uint64_t *state, int64_t capacity, bsr_t *out, void *ws, size_t ws_bytes,
+                                       void *stream);
+
+
 /* ---- the paper-faithful variant: 1 x b row segments, per-sample scope --------
  * (Table II geometry P:L180-197; "Blocks are only compared
  * locally, not among other activations in the mini-batch".)
@@ -278,6 +314,22 @@ BSR_API bsr_status_t bsr_act_block_sumsq(const void *Z, void *X_out, int64_t M, 
                                          int32_t act, void *ws, size_t ws_bytes, void *stream);
 BSR_API bsr_status_t bsr_prune_presummed(const void *X, int64_t M, int64_t K, int32_t b, int64_t k, int32_t dtype,
                                          bsr_t *out, void *ws, size_t ws_bytes, void *stream);
+
+
+/* ---- block-sparse affine scaling layer -------------------
+ * "A block-sparse version of the affine scaling layer found in ResMLP is now also
+ * available".  ResMLP's Aff(x) = alpha * x + beta scales each of the
+ * K channels of the M x K residual stream; with x saved as the BSR
+ * A of its top-k b x b blocks (bsr_prune), the scale gradient is
+ *   dalpha[J*b + c] (+)= sum over stored blocks (I, J), sum over r < b of
+ *                        values(I,J)[r][c] * dY[I*b + r][J*b + c]
+ * dY is M x K row-major (dy_dtype), dalpha K fp32.  (dbeta = column sums of dY
+ * and dX = alpha * dY need no activation.)  fp32 FMAs with round-to-nearest in a
+ * fixed order, split partials summed in split order: deterministic, graded at
+ * rel-F <= 1e-5.  Pruned blocks are never read.  ws: bsr_affine_wgrad_workspace_bytes. */
+BSR_API size_t bsr_affine_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b);
+BSR_API bsr_status_t bsr_affine_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, float *dalpha,
+                                      int32_t accumulate, void *ws, size_t ws_bytes, void *stream);
 
 
 /* Static description of a status code. */

@@ -33,6 +33,9 @@ other than itself:
                               fixture), brute force per sample, count
                               exactness per sample, numpy segment norms.
   wgrad_rect                  (X*mask)^T @ dY (numpy matmul) for 1 x b.
+  affine_wgrad                keep=1 -> numpy sum(X * dY, axis 0); any keep ->
+                              sum((X*mask) * dY, axis 0); keep=0 -> 0; a
+                              hand-computed 4 x 4 example.
 """
 from __future__ import annotations
 
@@ -88,6 +91,8 @@ def _load():
         lib.orc_wgrad_entries.restype = i32
         lib.orc_wgrad_entries.argtypes = [vp, vp, vp, i32, i64, i64, i64, i64, vp, i32, i64,
                                           vp, vp, i64, vp]
+        lib.orc_affine_wgrad.restype = i32
+        lib.orc_affine_wgrad.argtypes = [vp, vp, vp, i32, i64, i64, i64, i64, vp, i32, vp]
         _lib = lib
     return _lib
 
@@ -241,6 +246,20 @@ def wgrad_masked(rowptr, colidx, values, M: int, K: int, b: int, dY: np.ndarray)
     definition as `wgrad`, summed by BLAS instead of the quadruple loop."""
     Xm = _as_f64(decompress(rowptr, colidx, values, M, K, b))
     return Xm.T @ _as_f64(np.ascontiguousarray(dY))
+
+
+def affine_wgrad(rowptr, colidx, values, M: int, K: int, b: int, dY: np.ndarray) -> np.ndarray:
+    """fp64 scale gradient of the block-sparse affine layer:
+    dalpha[c] = sum over kept blocks of x * dY in column c (dY is M x K)."""
+    values = np.ascontiguousarray(values)
+    dY = np.ascontiguousarray(dY)
+    assert dY.shape == (M, K)
+    out = np.empty(K, dtype=np.float64)
+    _check(_load().orc_affine_wgrad(_ptr(np.ascontiguousarray(rowptr, np.int32)),
+                                    _ptr(np.ascontiguousarray(colidx, np.int32)), _ptr(values),
+                                    _dtype_code(values), M, K, b, b, _ptr(dY), _dtype_code(dY), _ptr(out)),
+           "affine_wgrad")
+    return out
 
 
 def wgrad_rect(rowptr, colidx, values, M: int, K: int, br: int, bc: int, dY: np.ndarray) -> np.ndarray:

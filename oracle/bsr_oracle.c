@@ -273,3 +273,27 @@ int orc_wgrad_entries(const int32_t *rowptr, const int32_t *colidx, const void *
     }
     return 0;
 }
+
+/* ---- block-sparse affine scaling layer ----------------------
+ * "A block-sparse version of the affine scaling layer found in ResMLP":
+ * Aff(x) = alpha * x + beta per channel; its scale gradient from the BSR of x,
+ *   dalpha[J*bc + c] = sum over stored blocks p=(I,J), sum over r < br of
+ *                      values[p][r][c] * dY[(I*br + r)][J*bc + c]
+ * dY is M x K (the shape of x), dalpha K entries (fp64). */
+int orc_affine_wgrad(const int32_t *rowptr, const int32_t *colidx, const void *values, int dtype,
+                     int64_t M, int64_t K, int64_t br, int64_t bc,
+                     const void *dY, int dy_dtype, double *dalpha)
+{
+    if (orc_num_blocks(M, K, br, bc) < 0) return -1;
+    int64_t nbr = M / br;
+    for (int64_t i = 0; i < K; ++i) dalpha[i] = 0.0;
+    for (int64_t I = 0; I < nbr; ++I)
+        for (int64_t p = rowptr[I]; p < rowptr[I + 1]; ++p) {
+            int64_t J = colidx[p];
+            for (int64_t r = 0; r < br; ++r)
+                for (int64_t c = 0; c < bc; ++c)
+                    dalpha[J * bc + c] += orc_elem(values, dtype, p * br * bc + r * bc + c) *
+                                          orc_elem(dY, dy_dtype, (I * br + r) * K + J * bc + c);
+        }
+    return 0;
+}

@@ -20,7 +20,7 @@ from . import _lib
 from ._lib import ALGO, BsrError, DT_BF16, DT_F32, PREC
 
 __all__ = ["BSR", "BsrError", "prune", "decompress", "wgrad", "block_sumsq", "num_blocks", "keep_count",
-           "storage_bytes", "workspace", "version", "set_pdl", "SparseLinear", "sparse_linear", "prune_global",
+           "storage_bytes", "workspace", "version", "set_pdl", "affine_wgrad", "SparseAffine", "SparseLinear", "sparse_linear", "prune_global",
            "RowBSR", "prune_rows", "decompress_rows", "wgrad_rows", "act_prune"]
 
 _DT = {torch.float32: DT_F32, torch.bfloat16: DT_BF16}
@@ -249,11 +249,30 @@ def wgrad(A: BSR, dY: torch.Tensor, prec: str = "fp32", out: torch.Tensor | None
     return out
 
 
+def affine_wgrad(A: BSR, dY: torch.Tensor, out: torch.Tensor | None = None, accumulate: bool = False,
+                 stream=None) -> torch.Tensor:
+    """Scale gradient of the block-sparse affine layer: dalpha[c] = sum of
+    x * dY over the kept blocks of column c (K fp32).  dY: M x K, like X."""
+    lib = _lib.load()
+    dY = _cuda2d(dY, "dY")
+    if tuple(dY.shape) != (A.M, A.K):
+        raise ValueError(f"dY must be {A.M} x {A.K} like the pruned activation, got {tuple(dY.shape)}")
+    if out is None:
+        out = torch.empty(A.K, dtype=torch.float32, device=dY.device)
+    else:
+        _check_dense_out(out, (A.K,), torch.float32, dY.device, "out")
+    ws = workspace(lib.bsr_affine_wgrad_workspace_bytes(A.M, A.K, A.b), dY.device, stream=stream)
+    cs = A.c_struct()
+    _lib.check(lib.bsr_affine_wgrad(ctypes.byref(cs), dY.data_ptr(), _dt(dY), out.data_ptr(), int(accumulate),
+                                    ws.data_ptr(), ws.numel(), _stream(stream)))
+    return out
+
+
 def set_pdl(mask: int) -> int:
     """Process-wide programmatic-dependent-launch mask (include/bsrprune.h); returns the old one."""
     return int(_lib.load().bsr_set_pdl(int(mask)))
 
 
-from .sparse_linear import SparseLinear, sparse_linear  # noqa: E402  (uses the functions above)
+from .sparse_linear import SparseAffine, SparseLinear, sparse_linear  # noqa: E402  (uses the functions above)
 from .global_select import prune_global  # noqa: E402
 from .rows import RowBSR, decompress_rows, prune_rows, wgrad_rows  # noqa: E402

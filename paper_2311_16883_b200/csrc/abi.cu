@@ -244,6 +244,82 @@ bsr_status_t bsr_prune_threshold(const void *X, int64_t M, int64_t K, int32_t b,
     return ok();
 }
 
+/* ---- device-side global selection (no host round trips; select_global.cu) ---- */
+size_t bsr_gselect_state_bytes(void) { return bsrp::kGStateWords * sizeof(uint64_t); }
+
+bsr_status_t bsr_gselect_init(int64_t k_total, uint64_t *state, void *stream) {
+    if (k_total < 0) return fail(BSR_ERR_INVALID_ARG, "k_total=%lld < 0", (long long)k_total);
+    if (!state) return fail(BSR_ERR_INVALID_ARG, "state is NULL");
+    return cuda_status(bsrp::launch_gselect_init(k_total, state, static_cast<cudaStream_t>(stream)), "bsr_gselect_init");
+}
+
+bsr_status_t bsr_gselect_hist(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype, int32_t level,
+                              const uint64_t *state, uint32_t *hist, void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_shape(M, K, b, dtype);
+    if (st != BSR_OK) return st;
+    if (level < 0 || level > 2) return fail(BSR_ERR_INVALID_ARG, "level=%d must be 0, 1 or 2", level);
+    if (!state || !hist) return fail(BSR_ERR_INVALID_ARG, "state or hist is NULL");
+    if (level == 0 && !X) return fail(BSR_ERR_INVALID_ARG, "X is NULL");
+    if (level == 0 && !aligned16(X)) return fail(BSR_ERR_ALIGNMENT, "X is not 16-byte aligned");
+    st = check_ws((M / b) * (K / b), ws, ws_bytes);
+    if (st != BSR_OK) return st;
+    return cuda_status(bsrp::launch_gselect_hist(X, M, K, b, elem_size(dtype), level, state, hist, ws,
+                                                 static_cast<cudaStream_t>(stream)),
+                       "bsr_gselect_hist launch");
+}
+
+bsr_status_t bsr_gselect_update(const uint32_t *hist_total, int32_t level, uint64_t *state, void *stream) {
+    if (level < 0 || level > 2) return fail(BSR_ERR_INVALID_ARG, "level=%d must be 0, 1 or 2", level);
+    if (!state || !hist_total) return fail(BSR_ERR_INVALID_ARG, "state or hist_total is NULL");
+    return cuda_status(bsrp::launch_gselect_update(hist_total, level, state, static_cast<cudaStream_t>(stream)),
+                       "bsr_gselect_update launch");
+}
+
+bsr_status_t bsr_gselect_counts(int64_t M, int64_t K, int32_t b, const uint64_t *state, uint64_t *counts, void *ws,
+                                size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_shape(M, K, b, BSR_DT_F32);
+    if (st != BSR_OK) return st;
+    if (!state || !counts) return fail(BSR_ERR_INVALID_ARG, "state or counts is NULL");
+    st = check_ws((M / b) * (K / b), ws, ws_bytes);
+    if (st != BSR_OK) return st;
+    return cuda_status(bsrp::launch_gselect_counts(M, K, b, state, counts, ws, static_cast<cudaStream_t>(stream)),
+                       "bsr_gselect_counts launch");
+}
+
+bsr_status_t bsr_gselect_take(const uint64_t *all_counts, int32_t world, int32_t rank, uint64_t *state, void *stream) {
+    if (world < 1 || rank < 0 || rank >= world)
+        return fail(BSR_ERR_INVALID_ARG, "rank=%d outside [0, world=%d)", rank, world);
+    if (!state || !all_counts) return fail(BSR_ERR_INVALID_ARG, "state or all_counts is NULL");
+    return cuda_status(bsrp::launch_gselect_take(all_counts, world, rank, state, static_cast<cudaStream_t>(stream)),
+                       "bsr_gselect_take launch");
+}
+
+bsr_status_t bsr_prune_gselect(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype, const uint64_t *state,
+                               int64_t capacity, bsr_t *out, void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_shape(M, K, b, dtype);
+    if (st != BSR_OK) return st;
+    const int64_t N = (M / b) * (K / b);
+    if (capacity < 0 || capacity > N)
+        return fail(BSR_ERR_INVALID_ARG, "capacity=%lld outside [0, N=%lld]", (long long)capacity, (long long)N);
+    if (!X || !state) return fail(BSR_ERR_INVALID_ARG, "X or state is NULL");
+    if (!out || !out->rowptr) return fail(BSR_ERR_INVALID_ARG, "output BSR descriptor / rowptr is NULL");
+    if (capacity > 0 && (!out->colidx || !out->values))
+        return fail(BSR_ERR_INVALID_ARG, "out->colidx / out->values are NULL with capacity=%lld", (long long)capacity);
+    if (!aligned16(X)) return fail(BSR_ERR_ALIGNMENT, "X is not 16-byte aligned");
+    if (capacity > 0 && !aligned16(out->values)) return fail(BSR_ERR_ALIGNMENT, "out->values is not 16-byte aligned");
+    st = check_ws(N, ws, ws_bytes);
+    if (st != BSR_OK) return st;
+    cudaError_t e = bsrp::launch_prune_threshold(X, M, K, b, elem_size(dtype), 0u, 0, 0u, capacity, out->rowptr,
+                                                 out->colidx, out->values, ws, static_cast<cudaStream_t>(stream), state);
+    if (e != cudaSuccess) return cuda_status(e, "bsr_prune_gselect launch");
+    out->M = M;
+    out->K = K;
+    out->b = b;
+    out->dtype = dtype;
+    out->nnzb = capacity;
+    return ok();
+}
+
 /* ---- paper-faithful 1 x b per-sample variant (prune_rows.cu) ---- */
 size_t bsr_prune_rows_workspace_bytes(int64_t M, int64_t K, int32_t b) {
     if (M <= 0 || K <= 0 || !supported_b(b) || K % b) return 0;
@@ -424,6 +500,34 @@ bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t
 }
 
 uint32_t bsr_set_pdl(uint32_t mask) { return bsrp::g_pdl.exchange(mask); }
+
+/* ---- block-sparse affine layer (affine.cu) ---- */
+size_t bsr_affine_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b) {
+    if (bsr_num_blocks(M, K, b) < 0 || !supported_b(b)) return 0;
+    return bsrp::affine_wgrad_ws_bytes(M, K, b);
+}
+
+bsr_status_t bsr_affine_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, float *dalpha, int32_t accumulate,
+                              void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_bsr(A);
+    if (st != BSR_OK) return st;
+    const int esy = elem_size(dy_dtype);
+    if (esy == 0) return fail(BSR_ERR_INVALID_ARG, "dy_dtype %d is not BSR_DT_F32 or BSR_DT_BF16", dy_dtype);
+    if (!dY || !dalpha) return fail(BSR_ERR_INVALID_ARG, "dY or dalpha is NULL");
+    if (accumulate != 0 && accumulate != 1) return fail(BSR_ERR_INVALID_ARG, "accumulate must be 0 or 1");
+    if (!aligned16(dY) || !aligned16(dalpha)) return fail(BSR_ERR_ALIGNMENT, "dY or dalpha is not 16-byte aligned");
+    if ((A->K * esy) % 16 != 0) return fail(BSR_ERR_ALIGNMENT, "row pitch of dY (K=%lld) is not a multiple of 16 bytes",
+                                            (long long)A->K);
+    const size_t need = bsrp::affine_wgrad_ws_bytes(A->M, A->K, A->b);
+    if (!ws || ws_bytes < need)
+        return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+    if (!aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
+    if (overlap(ws, need, dalpha, (size_t)A->K * 4)) return fail(BSR_ERR_INVALID_ARG, "workspace overlaps dalpha");
+    return cuda_status(bsrp::launch_affine_wgrad(A->rowptr, A->colidx, A->nnzb ? A->values : nullptr,
+                                                 elem_size(A->dtype), A->M, A->K, A->b, dY, esy, dalpha, accumulate,
+                                                 ws, static_cast<cudaStream_t>(stream)),
+                       "bsr_affine_wgrad launch");
+}
 
 const char *bsr_status_string(int32_t status) {
     switch (status) {

@@ -61,7 +61,16 @@ cudaError_t launch_select_counts(int64_t M, int64_t K, int b, uint32_t T, int sh
                                  cudaStream_t stream);
 cudaError_t launch_prune_threshold(const void *X, int64_t M, int64_t K, int b, int es, uint32_t T, int shift,
                                    uint32_t tie_take, int64_t k, int32_t *rowptr, int32_t *colidx, void *values,
-                                   void *ws, cudaStream_t stream);
+                                   void *ws, cudaStream_t stream, const uint64_t *gstate = nullptr);
+// Device-side global selection (select_global.cu): the protocol state lives in device memory.
+constexpr int kGStateWords = 16;
+cudaError_t launch_gselect_init(int64_t k_total, uint64_t *state, cudaStream_t stream);
+cudaError_t launch_gselect_hist(const void *X, int64_t M, int64_t K, int b, int es, int level, const uint64_t *state,
+                                uint32_t *hist, void *ws, cudaStream_t stream);
+cudaError_t launch_gselect_update(const uint32_t *hist_total, int level, uint64_t *state, cudaStream_t stream);
+cudaError_t launch_gselect_counts(int64_t M, int64_t K, int b, const uint64_t *state, uint64_t *counts, void *ws,
+                                  cudaStream_t stream);
+cudaError_t launch_gselect_take(const uint64_t *all_counts, int world, int rank, uint64_t *state, cudaStream_t stream);
 
 // Paper-faithful 1 x b per-sample variant (prune_rows.cu).
 cudaError_t launch_prune_rows(const void *X, int64_t M, int64_t K, int b, int es, int64_t S, int64_t ks,
@@ -94,6 +103,11 @@ size_t wgrad_span_ws_bytes(int64_t M, int64_t K, int b, int64_t N);
 cudaError_t launch_wgrad_span(const int32_t *rowptr, const int32_t *colidx, const void *values,
                               int64_t nnzb, int kind, int64_t M, int64_t K, int b, const void *dY,
                               int64_t N, float *dW, int accumulate, void *ws, cudaStream_t stream);
+// Block-sparse affine layer (affine.cu): dalpha[c] = sum over kept blocks of x * dY in column c.
+size_t affine_wgrad_ws_bytes(int64_t M, int64_t K, int b);
+cudaError_t launch_affine_wgrad(const int32_t *rowptr, const int32_t *colidx, const void *values, int es_x,
+                                int64_t M, int64_t K, int b, const void *dY, int es_y, float *dalpha,
+                                int accumulate, void *ws, cudaStream_t stream);
 // dW (+)= sum over nsplit partial K x N tiles in split order (deterministic).
 cudaError_t launch_splitk_reduce(const float *ws, float *dW, int64_t n, int nsplit, int accumulate,
                                  cudaStream_t stream);

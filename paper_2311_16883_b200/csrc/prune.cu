@@ -54,6 +54,7 @@ struct PruneParams {
     uint2 *cand;  // [kCandMax] (key, flat index) of the boundary bin's blocks
     int pdl_trig;   // 1: trigger the PDL successor before the pack phase
     int presummed;  // 1: block sums already in `sumsq` (act_sumsq_kernel); phase 1 skips X
+    const unsigned long long *gstate;  // device-side global selection (select_global.cu): T, shift, r, k from here
 };
 
 // Selection key of a block: fp32 bits of sumsq (>= 0, so the integer order is
@@ -481,6 +482,12 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_apply_kerne
     using G_ = Geo<ES, B>;
     __shared__ uint64_t s_warp[32];
     __shared__ uint32_t s_sel[4];
+    if (p.gstate) {  // threshold, digit shift, tie quota and kept count decided on the device (GS_* words)
+        T = (uint32_t)p.gstate[1];
+        shift = (int)p.gstate[2];
+        r = (uint32_t)p.gstate[6];
+        p.k = (int64_t)p.gstate[7];
+    }
     const int64_t u0 = (int64_t)blockIdx.x * p.units / gridDim.x;
     const int64_t u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
     auto flat_start = [&](int64_t u) -> int64_t {
@@ -877,8 +884,9 @@ cudaError_t launch_decompress(const int32_t *rowptr, const int32_t *colidx, cons
 
 cudaError_t launch_prune_threshold(const void *X, int64_t M, int64_t K, int b, int es, uint32_t T, int shift,
                                    uint32_t tie_take, int64_t k, int32_t *rowptr, int32_t *colidx, void *values,
-                                   void *ws, cudaStream_t stream) {
+                                   void *ws, cudaStream_t stream, const uint64_t *gstate) {
     PruneParams p{};
+    p.gstate = reinterpret_cast<const unsigned long long *>(gstate);
     p.X = X;
     p.K = K;
     p.nbr = M / b;
@@ -888,7 +896,7 @@ cudaError_t launch_prune_threshold(const void *X, int64_t M, int64_t K, int b, i
     p.rowptr = rowptr;
     p.colidx = colidx;
     p.values = values;
-    if (k == 0) return cudaMemsetAsync(rowptr, 0, (size_t)(p.nbr + 1) * 4, stream);
+    if (k == 0 && !gstate) return cudaMemsetAsync(rowptr, 0, (size_t)(p.nbr + 1) * 4, stream);
     const PruneWs w = prune_ws_layout(p.N);
     char *base = static_cast<char *>(ws);
     p.bar = reinterpret_cast<uint32_t *>(base + w.hdr);

@@ -305,7 +305,10 @@ struct Cfg {
     static constexpr uint32_t B_LAYOUT = TF32 ? 1u : BW == 128 ? 2u : BW == 64 ? 4u : 6u;  // SW128_32B / SW128 / SW64 / SW32
     static_assert(!TF32 || BW == 128, "tf32 MN-major operands need 128-byte block rows (b >= 32)");
     static constexpr int MAX_RUN = 256 / B;                 // blocks per MMA (N <= 256)
-    static constexpr int G = BLOCK_BYTES >= 8192 ? 1 : BLOCK_BYTES >= 2048 ? 4 : 8;  // blocks per B TMA
+    // blocks per B TMA (a row's kept blocks are loaded G at a time, the count rounded up to
+    // G slots); the FP32 grade loads them one by one: its B ring is half as deep (B_lo copy)
+    // and every rounded-up slot would also be split (measured faster)
+    static constexpr int G = X3 ? 1 : BLOCK_BYTES >= 8192 ? 1 : BLOCK_BYTES >= 2048 ? 4 : 8;
     // One pipeline step = R consecutive block rows (64 dY rows): one dY slab TMA,
     // one TMEM A buffer, one trip through every barrier.  The per-step
     // synchronisation (each mbarrier wait costs ~100 cycles even when the phase
@@ -759,10 +762,13 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
     } else if (C::X3 && warp >= C::SPLIT_W0) {
         // ------------------------------------------------ B splitters (FP32 grade)
         // Walk the B producer's step sequence; once a step's blocks have landed
-        // (`full`), rewrite every value x of its B-ring slots as hi(x) in place and
-        // write lo(x) at the same offset of the B_lo ring (element-wise, so the
-        // swizzled layout and the MMA descriptors carry over), then make the
-        // generic-proxy writes visible to the tensor core and arrive on `lofull`.
+        // (`full`), write lo(x) = x - hi(x) of every value x at the same offset of
+        // the B_lo ring (element-wise, so the swizzled layout and the MMA
+        // descriptors carry over), then make the generic-proxy writes visible to
+        // the tensor core and arrive on `lofull`.  hi(x) itself is not written:
+        // kind::tf32 reads an fp32 operand as its sign, exponent and top 10
+        // mantissa bits, i.e. exactly hi(x) (truncation; writing hi(x) explicitly
+        // gave bit-identical dW, R15/R17).
         const int sw = warp - C::SPLIT_W0;
         int j = 0;
         for (int c = 0; c < nchunks; ++c) {
@@ -780,13 +786,15 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
                 for (int q = 0; q < R; ++q) {
                     const uint2 sb = subs[st * R + q];
                     const int nd = (int)(sb.y >> 16);
-                    uint4 *hi = reinterpret_cast<uint4 *>(ringB + (size_t)(sb.y & 0xFFFFu) * C::BLOCK_BYTES);
-                    uint4 *lo = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(hi) + ringB_bytes);
+                    const uint32_t hi0 = smem_u32(ringB) + (sb.y & 0xFFFFu) * (uint32_t)C::BLOCK_BYTES;
+                    const uint32_t lo_off = (uint32_t)ringB_bytes;
                     const int n16 = nd * (C::BLOCK_BYTES / 16);
                     for (int i = sw * 32 + lane; i < n16; i += 32 * C::SPLITTERS) {
-                        const uint4 x = hi[i];
-                        hi[i] = make_uint4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-                        lo[i] = make_uint4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
+                        const uint32_t a = hi0 + (uint32_t)i * 16u;
+                        uint32_t x0, x1, x2, x3;
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(a));
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a + lo_off), "r"(tf32_lo(x0)),
+                                     "r"(tf32_lo(x1)), "r"(tf32_lo(x2)), "r"(tf32_lo(x3)) : "memory");
                     }
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1020,7 +1028,8 @@ static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms) {
     // A ring: 64 KB of dY slabs per SM, 2..kMaxSA stages; the rest of shared memory
     // goes to the B ring (measured: with fp32 blocks the B ring's depth, not the A
     // ring's, bounds the main loop)
-    pl.sa = std::max(2, std::min(kMaxSA, 65536 / C::SLAB));
+    // (FP32 grade: 2 stages, the B ring and its B_lo copy take the rest -- measured faster)
+    pl.sa = C::X3 ? 2 : std::max(2, std::min(kMaxSA, 65536 / C::SLAB));
     // B ring (FP32 grade: plus its B_lo copy of the same size)
     const int ring = (kSmemBudget - kFixedSmem - pl.sa * C::SLAB) / C::ACC_MULT;
     // largest kcol range whose accumulator(s) leave room for two A buffers in the

@@ -3,9 +3,9 @@ largest blocks of the CONCATENATED activation of all data-parallel ranks, so the
 multi-GPU kept set equals the single-GPU one (P:L413-418 applied to the whole
 batch; tie rule BJ: lower flat index first = lower rank first).
 
-The device work is the library's (include/bsrprune.h: bsr_select_hist,
-bsr_select_counts, bsr_prune_threshold).  This module only runs the exchange
-protocol between those calls with torch.distributed:
+The device work is the library's (include/bsrprune.h: bsr_gselect_*, the
+protocol state in device memory).  This module only issues the collectives
+between those calls with torch.distributed:
 
   1. level-0 digit histogram (key bits 30..19) per rank  -> all-reduce -> boundary bin
   2. while the boundary bin is split: next digit (bits 18..9, then 8..0) of the
@@ -14,8 +14,10 @@ protocol between those calls with torch.distributed:
   4. tie quota: r = k - sum(above); rank q keeps its first
      clamp(r - ties on ranks < q, 0, ties_q) tied blocks -> k_q = above_q + that.
 
-`threshold_protocol` is the pure host logic (injected histogram / count /
-collective callables), unit-tested on CPU with gloo at world size 2.
+`threshold_protocol` is the same protocol as pure host logic (injected
+histogram / count / collective callables), unit-tested on CPU with gloo at world
+size 2 and brute force; the device kernels follow it step by step
+(csrc/select_global.cu, gselect_*).
 """
 from __future__ import annotations
 
@@ -71,13 +73,19 @@ def threshold_protocol(k_total: int, rank: int, hist_fn: Callable[[int, int], np
     return prefix, shift, tie_take, int(above_q) + tie_take
 
 
-def prune_global(X, b: int, keep: float, group=None, stream=None):
+def prune_global(X, b: int, keep: float, group=None, stream=None, total_rows: int | None = None):
     """bsr_prune with the whole data-parallel batch as selection scope.  Every rank
-    calls it with its own rows; returns this rank's BSR (k_rank blocks)."""
+    calls it with its own rows; returns this rank's BSR (k_rank blocks).
+
+    The protocol runs with its state in device memory (bsr_gselect_*): three
+    histogram all-reduces and one all-gather on device buffers (NCCL; gloo stages
+    through the host), no device->host copy until this rank's kept count is read
+    at the very end to size the result.  total_rows: rows of the whole batch (the
+    caller's sharding plan knows it); if None it is all-reduced once on the host."""
     import torch
     import torch.distributed as dist
 
-    from . import _lib, _dt, _stream, alloc_bsr, keep_count, num_blocks, workspace
+    from . import BSR, _dt, _lib, _stream, alloc_bsr, keep_count, num_blocks, workspace
 
     lib = _lib.load()
     M, K = X.shape
@@ -89,44 +97,53 @@ def prune_global(X, b: int, keep: float, group=None, stream=None):
     ws = workspace(ws_bytes, dev, kind="prune", stream=stream)
     st = _stream(stream)
 
-    def coll_tensor(a: np.ndarray):
-        t = torch.from_numpy(np.ascontiguousarray(a))
-        return t if cpu_coll else t.to(dev)
-
-    def allreduce(a):
+    def allreduce_(t):  # in place, on device buffers (gloo: through the host)
         if world == 1:
-            return a
-        t = coll_tensor(a)
-        dist.all_reduce(t, group=group)
-        return t.cpu().numpy()
+            return t
+        if cpu_coll:
+            h = t.cpu()
+            dist.all_reduce(h, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, group=group)
+        return t
 
-    def allgather(a):
+    def allgather(t):
         if world == 1:
-            return a[None]
-        t = coll_tensor(a)
-        out = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(out, t, group=group)
-        return np.stack([o.cpu().numpy() for o in out])
+            return t.reshape(1, -1).clone()
+        src = t.cpu() if cpu_coll else t
+        outs = [torch.empty_like(src) for _ in range(world)]
+        dist.all_gather(outs, src, group=group)
+        return torch.stack(outs).to(dev)
 
-    def hist_fn(level, prefix):
-        n = (4096, 1024, 512)[level]
-        h = torch.empty(n, dtype=torch.int32, device=dev)
-        _lib.check(lib.bsr_select_hist(X.data_ptr(), M, K, b, _dt(X), level, prefix, h.data_ptr(), ws.data_ptr(),
-                                       ws.numel(), st))
-        return h.cpu().numpy().astype(np.int64)
-
-    def counts_fn(threshold, shift):
-        c = torch.empty(2, dtype=torch.int64, device=dev)
-        _lib.check(lib.bsr_select_counts(M, K, b, threshold, shift, c.data_ptr(), ws.data_ptr(), ws.numel(), st))
-        return tuple(int(v) for v in c.cpu().tolist())
-
-    n_total = int(allreduce(np.asarray([num_blocks(M, K, b)], dtype=np.int64))[0])
+    N_rank = num_blocks(M, K, b)
+    if total_rows is None:
+        n_total = N_rank
+        if world > 1:
+            t = torch.tensor([N_rank], dtype=torch.int64)
+            if not cpu_coll:
+                t = t.to(dev)
+            dist.all_reduce(t, group=group)
+            n_total = int(t.item())
+    else:
+        n_total = num_blocks(int(total_rows), K, b)
     k_total = keep_count(n_total, keep)
-    if k_total == 0:
-        hist_fn(0, 0)  # (the sums are not needed; keep the call sequence uniform across ranks)
-    thr, shift, tie_take, k_rank = threshold_protocol(k_total, rank, hist_fn, counts_fn, allreduce, allgather)
-    out = alloc_bsr(M, K, b, k_rank, X.dtype, dev)
+    state = torch.empty(lib.bsr_gselect_state_bytes() // 8, dtype=torch.int64, device=dev)
+    _lib.check(lib.bsr_gselect_init(k_total, state.data_ptr(), st))
+    for level, nb in enumerate((4096, 1024, 512)):
+        hist = torch.empty(nb, dtype=torch.int32, device=dev)  # uint32 counts (< 2^31)
+        _lib.check(lib.bsr_gselect_hist(X.data_ptr(), M, K, b, _dt(X), level, state.data_ptr(), hist.data_ptr(),
+                                        ws.data_ptr(), ws.numel(), st))
+        allreduce_(hist)
+        _lib.check(lib.bsr_gselect_update(hist.data_ptr(), level, state.data_ptr(), st))
+    counts = torch.empty(2, dtype=torch.int64, device=dev)
+    _lib.check(lib.bsr_gselect_counts(M, K, b, state.data_ptr(), counts.data_ptr(), ws.data_ptr(), ws.numel(), st))
+    allc = allgather(counts).contiguous()
+    _lib.check(lib.bsr_gselect_take(allc.data_ptr(), world, rank, state.data_ptr(), st))
+    cap = min(N_rank, k_total)
+    out = alloc_bsr(M, K, b, cap, X.dtype, dev)
     cs = out.c_struct()
-    _lib.check(lib.bsr_prune_threshold(X.data_ptr(), M, K, b, _dt(X), thr, shift, tie_take, k_rank, ctypes.byref(cs),
-                                       ws.data_ptr(), ws.numel(), st))
-    return out
+    _lib.check(lib.bsr_prune_gselect(X.data_ptr(), M, K, b, _dt(X), state.data_ptr(), cap, ctypes.byref(cs),
+                                     ws.data_ptr(), ws.numel(), st))
+    k_rank = int(state[7].item())  # the one device -> host read: the size of this rank's result
+    return BSR(rowptr=out.rowptr, colidx=out.colidx[:k_rank], values=out.values[:k_rank], M=M, K=K, b=b)

@@ -22,9 +22,9 @@ import math
 
 import torch
 
-from . import BSR, prune, wgrad
+from . import BSR, affine_wgrad, prune, wgrad
 
-__all__ = ["SparseLinear", "sparse_linear"]
+__all__ = ["SparseLinear", "sparse_linear", "SparseAffine"]
 
 
 class _SparseLinearFn(torch.autograd.Function):
@@ -109,3 +109,48 @@ class SparseLinear(torch.nn.Module):
     def extra_repr(self) -> str:
         return (f"in_features={self.in_features}, out_features={self.out_features}, sparsity={self.sparsity}, "
                 f"block={self.block}, bias={self.bias is not None}")
+
+
+class _SparseAffineFn(torch.autograd.Function):
+    """y = alpha * x + beta per channel; x saved as the BSR of its top-k blocks."""
+
+    @staticmethod
+    def forward(ctx, x2d: torch.Tensor, alpha: torch.Tensor, beta: torch.Tensor, keep: float, block: int):
+        y = torch.addcmul(beta, x2d, alpha)
+        ctx.bsr = prune(x2d.detach(), block, keep=keep)
+        ctx.save_for_backward(alpha)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy: torch.Tensor):
+        (alpha,) = ctx.saved_tensors
+        dy = dy.contiguous()
+        dx = dy * alpha if ctx.needs_input_grad[0] else None
+        dalpha = affine_wgrad(ctx.bsr, dy).to(alpha.dtype) if ctx.needs_input_grad[1] else None
+        dbeta = dy.sum(0) if ctx.needs_input_grad[2] else None
+        ctx.bsr = None
+        return dx, dalpha, dbeta, None, None
+
+
+class SparseAffine(torch.nn.Module):
+    """ResMLP's affine scaling layer Aff(x) = alpha * x + beta in its
+    block-sparse version: the input activation is saved as the BSR of
+    its round((1 - s) * N) largest-l2-norm b x b blocks and the scale gradient is
+    computed from it (bsr_affine_wgrad); dx = alpha * dy and dbeta = sum(dy) need
+    no activation and stay dense."""
+
+    def __init__(self, dim: int, sparsity: float = 0.5, block: int = 16, device=None, dtype=None):
+        super().__init__()
+        if dim % block:
+            raise ValueError(f"dim={dim} must be a multiple of block={block}")
+        self.dim, self.sparsity, self.block = dim, float(sparsity), int(block)
+        self.alpha = torch.nn.Parameter(torch.ones(dim, device=device, dtype=dtype))
+        self.beta = torch.nn.Parameter(torch.zeros(dim, device=device, dtype=dtype))
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if not self.training or not torch.is_grad_enabled():
+            return torch.addcmul(self.beta, x, self.alpha)
+        lead = x.shape[:-1]
+        x2d = x.reshape(-1, self.dim).contiguous()
+        y = _SparseAffineFn.apply(x2d, self.alpha, self.beta, 1.0 - self.sparsity, self.block)
+        return y.reshape(*lead, self.dim)

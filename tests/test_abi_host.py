@@ -161,3 +161,29 @@ def test_variant_calls_validation(lib):
     assert lib.bsr_act_block_sumsq(FAKE, FAKE + 8, 256, 256, 16, 0, 1, WS, BIG, None) == 4   # alignment
     assert lib.bsr_act_block_sumsq(FAKE, FAKE, 256, 256, 16, 0, 1, WS, 8, None) == 5         # workspace
     assert lib.bsr_prune_presummed(FAKE, 256, 256, 16, 10, 0, ctypes.byref(out), None, 0, None) == 5
+
+
+def test_wgrad_algo_set_pdl_and_affine_validation(lib):
+    """bsr_wgrad_algo (explicit kernel family), bsr_set_pdl and the block-sparse
+    affine layer's entry point: host-side checks before any launch."""
+    good = _lib.BsrT(256, 256, 16, 0, 10, FAKE, FAKE, FAKE)
+    W, WS, BIG = FAKE + 0x1000000, FAKE + 0x800000, 1 << 30
+    assert lib.bsr_wgrad_algo(ctypes.byref(good), FAKE, 0, 256, W, 0, 0, 7, WS, BIG, None) == 1    # algo
+    assert lib.bsr_wgrad_algo(ctypes.byref(good), FAKE, 0, 256, W, 0, 1, 3, WS, BIG, None) == 3    # tf32 on FFMA
+    assert lib.bsr_wgrad_algo(ctypes.byref(good), FAKE, 0, 256, W, 0, 0, 2, WS, BIG, None) == 3    # fp32 on span
+    assert lib.bsr_wgrad_algo(ctypes.byref(good), FAKE, 0, 256, W, 0, 0, 1, WS, BIG, None) == 3    # fp32 runs b=16
+    assert lib.bsr_wgrad_algo(ctypes.byref(good), FAKE, 0, 256, W, 0, 1, 1, WS, BIG, None) == 3    # tf32 runs b=16
+    b32 = _lib.BsrT(25088, 384, 32, 0, 4704, FAKE, FAKE, FAKE)
+    need = lib.bsr_wgrad_workspace_bytes(25088, 384, 32, 1536, 0)
+    assert need >= 17 * 384 * 1536 * 4  # FP32 grade: the chain cap sets >= 17 splits at C2
+    W2, WS2 = FAKE + (1 << 30), FAKE + (1 << 31)  # clear of dY (154 MB)
+    assert lib.bsr_wgrad_algo(ctypes.byref(b32), FAKE, 0, 1536, W2, 0, 0, 1, WS2, need - 16, None) == 5  # workspace
+    old = lib.bsr_set_pdl(0)
+    assert lib.bsr_set_pdl(old) == 0
+    assert lib.bsr_affine_wgrad_workspace_bytes(256, 256, 16) > 0
+    assert lib.bsr_affine_wgrad_workspace_bytes(256, 256, 12) == 0
+    assert lib.bsr_affine_wgrad(None, FAKE, 0, W, 0, WS, BIG, None) == 1
+    assert lib.bsr_affine_wgrad(ctypes.byref(good), FAKE, 5, W, 0, WS, BIG, None) == 1             # dy dtype
+    assert lib.bsr_affine_wgrad(ctypes.byref(good), FAKE, 0, W, 3, WS, BIG, None) == 1             # accumulate
+    assert lib.bsr_affine_wgrad(ctypes.byref(good), FAKE + 4, 0, W, 0, WS, BIG, None) == 4         # alignment
+    assert lib.bsr_affine_wgrad(ctypes.byref(good), FAKE, 0, W, 0, WS, 16, None) == 5             # workspace

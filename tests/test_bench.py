@@ -38,3 +38,14 @@ def test_native_arm_gpu():
     assert d["gpu_launches"] == per_step["step"] * 20
     assert 0 < d["roofline"]["frac"] < 1.5
     assert d["e2e"]["h2d_bytes_per_step"] == 25088 * 384 * 4 + 25088 * 1536 * 4
+
+
+@pytest.mark.gpu
+def test_native_arm_c4_one_gpu():
+    """--config C4 (ResMLP-B24, 24 x (fc1, fc2), strong scaling) at one rank: a smaller
+    keep keeps it quick; every layer's prune, decompress and dW run each step."""
+    d = run_bench("--config", "C4", "--steps", "3", "--warmup", "3", "--keep", "0.2", timeout=900)
+    assert d["scaling"] == "strong" and d["n_gpus"] == 1
+    assert d["config"]["rows_per_rank"] == 1024 * 196
+    assert d["gpu_launches_per_step"] >= 48 * 3
+    assert d["value"] > 0 and d["ms_per_step"] > 0

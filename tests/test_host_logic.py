@@ -121,3 +121,56 @@ def test_gloo_two_ranks_allreduce_equals_concatenated_oracle():
         assert tmax == 2.0 and tsum == 3.0
     # per-rank scope (R2): each rank keeps nearest(keep * its own block count)
     assert mask.sum() == sum(oracle.keep_count(oracle.num_blocks(M // 2, K, b), keep) for _ in range(2))
+
+
+def test_plan_buckets():
+    assert D.plan_buckets([10, 10, 10, 10], 25) == [[0, 1], [2, 3]]
+    assert D.plan_buckets([30, 5, 5], 25) == [[0], [1, 2]]  # an oversized gradient gets its own bucket
+    assert D.plan_buckets([], 8) == []
+    sizes = [9437184] * 48  # ResMLP-B24: 24 x (fc1, fc2) dW of 768 x 3072 fp32
+    b = D.plan_buckets(sizes, 40 << 20)
+    assert [i for bk in b for i in bk] == list(range(48))  # order preserved, every gradient once
+    assert all(sum(sizes[i] for i in bk) <= 40 << 20 for bk in b)
+    with pytest.raises(ValueError):
+        D.plan_buckets([1], 0)
+
+
+def _bucket_worker(rank, world, port, shapes, cap, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    D.init("gloo")
+    br = D.BucketedAllReduce(shapes, "cpu", cap_bytes=cap, dtype=torch.float64)
+    rng = np.random.default_rng(100 + rank)
+    local = []
+    for i, (k, n) in enumerate(shapes):  # "backward": write each gradient, then mark it ready
+        g = torch.from_numpy(rng.standard_normal((k, n)))
+        br.view(i).copy_(g)
+        local.append(g.clone())
+        br.ready(i)
+    br.wait()
+    q.put((rank, [br.view(i).clone().numpy() for i in range(len(shapes))], [g.numpy() for g in local],
+           len(br.buckets)))
+    D.finalize()
+
+
+def test_gloo_two_ranks_bucketed_allreduce():
+    """The bucket scheduler (a7 overlapped with the backward pass) at world size 2:
+    every gradient ends up as the sum over ranks, whatever bucket it sat in."""
+    shapes = [(8, 16), (4, 4), (16, 16), (2, 8), (8, 8)]
+    cap = 8 * 16 * 8  # bytes: float64 views, so ~1-2 gradients per bucket
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bucket_worker, args=(r, world, port, shapes, cap, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][3] >= 3  # several buckets were in flight
+    for i in range(len(shapes)):
+        want = res[0][2][i] + res[1][2][i]
+        for r in range(world):
+            np.testing.assert_allclose(res[r][1][i], want, rtol=1e-15, atol=0)

@@ -329,6 +329,37 @@ def test_wgrad_masked_equals_quadruple_loop(bf16, keep):
         assert not oracle.wgrad_masked(*args).any()
 
 
+@pytest.mark.parametrize("keep", [0.0, 0.4, 1.0])
+def test_affine_wgrad_equals_masked_column_dot(keep):
+    """Block-sparse affine layer (P:L642-644): dalpha = sum over rows of (X*mask) * dY;
+    keep = 1 -> the dense affine gradient sum(X * dY, axis 0)."""
+    M, K, b = 96, 64, 16
+    X = synth.f_aff(M, K, seed=14)
+    dY = synth.grad_out(M, K, seed=14)
+    out = oracle.prune(X, b, oracle.keep_count(oracle.num_blocks(M, K, b), keep))
+    mask = np.kron(out["mask"].reshape(M // b, K // b), np.ones((b, b)))
+    ref = (X.astype(np.float64) * mask * dY.astype(np.float64)).sum(axis=0)
+    got = oracle.affine_wgrad(out["rowptr"], out["colidx"], out["values"], M, K, b, dY)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-15)
+    if keep == 1.0:
+        np.testing.assert_allclose(got, (X.astype(np.float64) * dY).sum(0), rtol=1e-12, atol=1e-15)
+    if keep == 0.0:
+        assert not got.any()
+
+
+def test_affine_wgrad_hand_example():
+    """The 4 x 4 worked example (b = 2, keep 0.75: kept B00, B01, B11) with dY = 1:
+    dalpha = column sums of the masked X = [3, 4+1... ] computed by hand."""
+    X = np.array([[3, 4, 0, 0], [0, 0, 1, 0], [0, 0, 2, 2], [0, 1, 2, 2]], np.float32)
+    out = oracle.prune(X, 2, 3)
+    got = oracle.affine_wgrad(out["rowptr"], out["colidx"], out["values"], 4, 4, 2, np.ones((4, 4), np.float32))
+    # masked X = [[3,4,0,0],[0,0,1,0],[0,0,2,2],[0,0,2,2]] (B10 = [[0,0],[0,1]] pruned)
+    np.testing.assert_array_equal(got, [3.0, 4.0, 5.0, 4.0])
+    dY = np.array([[1, 2, 3, 4]] * 4, np.float32)  # per-column weights
+    got = oracle.affine_wgrad(out["rowptr"], out["colidx"], out["values"], 4, 4, 2, dY)
+    np.testing.assert_array_equal(got, [3.0, 8.0, 15.0, 16.0])
+
+
 def test_rel_frobenius():
     B = np.array([[3.0, 4.0]])
     assert oracle.rel_frobenius(B, B) == 0.0
