@@ -14,8 +14,10 @@ void count_launch(uint64_t n = 1);
 // PDL launches.  pdl_flags() = the bsr_set_pdl bit mask (0: plain stream order):
 //   1 prune triggers before its pack phase, 2 wgrad triggers at its start,
 //   4 wgrad triggers at its epilogue, 8 split-K reduce triggers at its start,
-//   16 / 32 / 64 PDL attribute on the wgrad / reduce / decompress launches.
-constexpr int kPdlDefault = 1 | 4 | 16 | 32 | 64;  // measured best; bit 8 was slower
+//   16 / 32 / 64 PDL attribute on the wgrad / reduce / decompress launches,
+//   128 PDL attribute on the small-N prune's first kernel (its second kernel always
+//   chains to the first with PDL: they form one operation).
+constexpr int kPdlDefault = 1 | 4 | 16 | 32 | 64 | 128;  // measured; bit 8 was slower
 int pdl_flags();
 // Launch `kern` with programmatic stream serialization: the kernel MUST call
 // pdl_wait() (common.cuh) before touching global memory.

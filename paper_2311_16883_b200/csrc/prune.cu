@@ -474,6 +474,145 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_kernel(Prun
     __syncthreads();
 }
 
+// ------------------------------------------------------------------ small-N path
+// Two plain (non-cooperative) launches chained with programmatic dependent
+// launch instead of one cooperative kernel with grid barriers, for N <= kSmallN
+// keys (S12 fc1/fc2 at b >= 16-32, B24 per-rank fc1): the kernel boundary is the
+// only grid-wide synchronisation, and PDL hides each launch behind its
+// predecessor's tail.
+//   prune_sums_kernel : phase 1 of prune_kernel (same units, same reduction tree,
+//                       so bit-identical block sums) + the level-1 histogram.
+//   prune_finish_kernel: every CTA loads the global histogram and ALL N keys into
+//                       shared memory, resolves the exact threshold (the
+//                       boundary bin refined by two more digits over the keys in
+//                       shared memory -- no candidate list, no overflow case),
+//                       counts the (above, tie) keys before its own flat range
+//                       from shared memory, then scans and packs its range as
+//                       prune_kernel does.  No grid barrier.
+constexpr int64_t kSmallN = 40960;  // keys held in shared memory by every finishing CTA (160 KB)
+
+template <int ES, int B>
+__global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_sums_kernel(PruneParams p) {
+    using G_ = Geo<ES, B>;
+    __shared__ uint32_t s_hist[kH1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kThreads / 32;
+    const int j = lane / G_::LPB, sub = lane % G_::LPB;
+    for (int i = threadIdx.x; i < kH1; i += kThreads) s_hist[i] = 0;
+    __syncthreads();
+    pdl_wait();  // launched with PDL: the predecessor (e.g. the previous step) has completed
+    if (p.presummed) {
+        for (int64_t f = (int64_t)blockIdx.x * kThreads + threadIdx.x; f < p.N; f += (int64_t)gridDim.x * kThreads)
+            atomicAdd(&s_hist[key_of(p.sumsq[f]) >> 19], 1u);
+    } else {
+        for (int64_t u = (int64_t)blockIdx.x * nw + wid; u < p.units; u += (int64_t)gridDim.x * nw) {
+            const int64_t I = u / p.upr, J = (u % p.upr) * G_::G + j;
+            const bool valid = J < p.nbc;
+            const float sq = block_sumsq_warp<ES, B>(p.X, p.K, I, J, sub, valid);
+            if (valid && sub == 0) {
+                p.sumsq[I * p.nbc + J] = sq;
+                atomicAdd(&s_hist[key_of(sq) >> 19], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kH1; i += kThreads)
+        if (s_hist[i]) atomicAdd(p.hist1 + i, s_hist[i]);
+    pdl_trigger();  // the finishing kernel may become resident; it waits for this grid's completion
+}
+
+template <int ES, int B>
+__global__ void __launch_bounds__(kThreads, 1) prune_finish_kernel(PruneParams p) {
+    extern __shared__ uint32_t s_key[];  // [N] key bits, flat order
+    __shared__ uint32_t s_h2[1024];
+    __shared__ uint64_t s_warp[32];
+    __shared__ uint32_t s_sel[4];
+    using G_ = Geo<ES, B>;
+    const int lane = threadIdx.x & 31;
+    const int64_t u0 = (int64_t)blockIdx.x * p.units / gridDim.x;
+    const int64_t u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
+    auto flat_start = [&](int64_t u) -> int64_t {
+        return u >= p.units ? p.N : (u / p.upr) * p.nbc + (u % p.upr) * G_::G;
+    };
+    const int64_t f0 = flat_start(u0), f1 = flat_start(u1);
+    const int N = (int)p.N;
+    pdl_wait();  // the sums kernel has completed: sumsq and hist1 are final
+    // boundary bin of the first digit from the global histogram
+    const uint32_t k = (uint32_t)p.k;
+    select_bin(p.hist1, kH1, k, s_warp, s_sel);
+    uint32_t prefix = s_sel[0], above = s_sel[1], bincnt = s_sel[2];
+    // every key into shared memory (16-byte loads, several in flight per thread)
+    {
+        const float4 *src = reinterpret_cast<const float4 *>(p.sumsq);
+        const int n4 = N / 4;
+        for (int i0 = threadIdx.x; i0 < n4; i0 += 4 * kThreads) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = i0 + u * kThreads < n4 ? __ldcg(src + i0 + u * kThreads) : float4{};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i0 + u * kThreads < n4)
+                    reinterpret_cast<uint4 *>(s_key)[i0 + u * kThreads] =
+                        make_uint4(key_of(v[u].x), key_of(v[u].y), key_of(v[u].z), key_of(v[u].w));
+        }
+        for (int f = n4 * 4 + threadIdx.x; f < N; f += kThreads) s_key[f] = key_of(__ldcg(p.sumsq + f));
+    }
+    // self-cleaning workspace: this CTA is done with hist1; the last one zeroes it
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_sel[3] = atomicAdd(p.bar + 32, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_sel[3]) {
+        __threadfence();
+        for (int i = threadIdx.x; i < kH1; i += kThreads) p.hist1[i] = 0;
+        if (threadIdx.x == 0) p.bar[32] = 0;
+    }
+    // refine the boundary bin over the keys in shared memory: bits 18..9, then 8..0
+    int shift = 19;
+    uint32_t r = k - above;
+    for (int pass = 0; pass < 2 && r < bincnt; ++pass) {
+        const int w = pass == 0 ? 10 : 9;
+        const int nshift = shift - w;
+        for (int i = threadIdx.x; i < (1 << w); i += kThreads) s_h2[i] = 0;
+        __syncthreads();
+        for (int fb = 0; fb < N; fb += kThreads) {
+            const int f = fb + threadIdx.x;
+            const uint32_t key = f < N ? s_key[f] : 0u;
+            const bool in = f < N && (key >> shift) == prefix;
+            const uint32_t bin = (key >> nshift) & ((1u << w) - 1u);
+            const uint32_t im = __ballot_sync(0xffffffffu, in);
+            if (!im) continue;
+            const int l0 = __ffs(im) - 1;
+            const uint32_t b0 = __shfl_sync(0xffffffffu, bin, l0);
+            if (__all_sync(0xffffffffu, !in || bin == b0)) {  // a warp of ties adds once
+                if (lane == l0) atomicAdd(&s_h2[b0], (uint32_t)__popc(im));
+            } else if (in) {
+                atomicAdd(&s_h2[bin], 1u);
+            }
+        }
+        __syncthreads();
+        select_bin<false>(s_h2, 1 << w, r, s_warp, s_sel);
+        prefix = (prefix << w) | s_sel[0];
+        above += s_sel[1];
+        bincnt = s_sel[2];
+        shift = nshift;
+        r = k - above;
+    }
+    // (above, tie) counts of every block before this CTA's range
+    uint32_t na = 0, nt = 0;
+    for (int64_t f = threadIdx.x; f < f0; f += kThreads) {
+        const uint32_t kk = s_key[f] >> shift;
+        na += kk > prefix;
+        nt += kk == prefix;
+    }
+    uint64_t pre;
+    block_excl_scan(((uint64_t)na << 32) | nt, s_warp, pre);
+    scan_and_index(p, f0, f1, pre, prefix, shift, r, s_warp);
+    if (p.pdl_trig) pdl_trigger();
+    pack_kept<ES, B>(p, u0, u1);
+}
+
 // Pack with a threshold chosen elsewhere (cross-rank global top-k, select_global.cu):
 // keep keys (>> shift) > T and the first `r` keys == T in flat order.  The block
 // sums of squares are already in the workspace (bsr_select_hist level 0).
@@ -767,8 +906,21 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
         count_launch();
         return cudaGetLastError();
     }
-    // (no per-launch memset: the kernel leaves its workspace header zeroed, see above)
+    // (no per-launch memset: the kernels leave their workspace header zeroed, see above)
     cudaError_t e = cudaSuccess;
+    if (p.N <= kSmallN) {
+        const size_t smem = (size_t)((p.N + 3) & ~int64_t(3)) * 4;
+        e = cudaFuncSetAttribute(prune_finish_kernel<ES, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        const int64_t per = kThreads / 32;  // one unit per warp
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((p.units + per - 1) / per, (int64_t)num_sms()));
+        e = launch_pdl(pdl_flags() & 128, prune_sums_kernel<ES, B>, dim3((unsigned)grid), dim3(kThreads), 0, stream, p);
+        if (e != cudaSuccess) return e;
+        count_launch();
+        e = launch_pdl(true, prune_finish_kernel<ES, B>, dim3((unsigned)grid), dim3(kThreads), smem, stream, p);
+        count_launch();
+        return e != cudaSuccess ? e : cudaGetLastError();
+    }
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, prune_kernel<ES, B>, kThreads, 0);
     if (e != cudaSuccess) return e;

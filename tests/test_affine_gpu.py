@@ -58,7 +58,7 @@ def test_affine_wgrad_s12_size():
 def test_sparse_affine_module():
     """SparseAffine: forward dense (alpha * x + beta), backward dx = alpha * dy and
     dbeta = sum(dy) dense, dalpha from the BSR of x."""
-    M, K, b = 196 * 4, 384, 32
+    M, K, b = 196 * 8, 384, 32
     layer = bp.SparseAffine(K, sparsity=0.5, block=b, device="cuda")
     with torch.no_grad():
         layer.alpha.copy_(torch.linspace(0.5, 1.5, K))
