@@ -200,6 +200,21 @@ BSR_API bsr_status_t bsr_wgrad_algo(const bsr_t *A, const void *dY, int32_t dy_d
                                     int32_t accumulate, int32_t prec, int32_t algo, void *ws, size_t ws_bytes,
                                     void *stream);
 
+/* dW with the data-parallel sum fused into it (a7 over NVLink
+ * SHARP): mc_dW is the MULTIMEM (NVLS multicast) address of a K x N fp32 buffer
+ * bound on every rank (e.g. torch symmetric memory's multicast_ptr); this rank's
+ * dW = X_bsr^T . dY is ADDED into it with multimem.red.add.f32 -- from the dW
+ * epilogue when the rows are not split, else from the split-K reduce -- so the
+ * NVSwitch sums the ranks' contributions and every rank's copy holds the total.
+ * The caller zeroes the buffer on every rank before and synchronises the ranks
+ * after (the adds are asynchronous).  Per-run tensor-core kernel only (prec
+ * TF32, BF16 or the FP32 grade, algo AUTO or TC_RUNS, as bsr_wgrad_algo);
+ * otherwise BSR_ERR_UNSUPPORTED.  With one rank and a zeroed buffer the result
+ * is bit-identical to bsr_wgrad (0 + x = x).  The ranks' sum is not
+ * order-deterministic. */
+BSR_API bsr_status_t bsr_wgrad_multicast(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *mc_dW,
+                                         int32_t prec, int32_t algo, void *ws, size_t ws_bytes, void *stream);
+
 /* Programmatic-dependent-launch mask of this process (bit meanings in
  * csrc/launch.h; 0 = plain stream order).  Returns the previous mask.  Results
  * are bit-identical for every mask (tests/test_pdl_gpu.py); only the overlap

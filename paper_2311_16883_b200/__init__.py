@@ -20,7 +20,7 @@ from . import _lib
 from ._lib import ALGO, BsrError, DT_BF16, DT_F32, PREC
 
 __all__ = ["BSR", "BsrError", "prune", "decompress", "wgrad", "block_sumsq", "num_blocks", "keep_count",
-           "storage_bytes", "workspace", "version", "set_pdl", "affine_wgrad", "SparseAffine", "SparseLinear", "sparse_linear", "prune_global",
+           "storage_bytes", "workspace", "version", "set_pdl", "wgrad_multicast", "affine_wgrad", "SparseAffine", "SparseLinear", "sparse_linear", "prune_global",
            "RowBSR", "prune_rows", "decompress_rows", "wgrad_rows", "act_prune"]
 
 _DT = {torch.float32: DT_F32, torch.bfloat16: DT_BF16}
@@ -266,6 +266,27 @@ def affine_wgrad(A: BSR, dY: torch.Tensor, out: torch.Tensor | None = None, accu
     _lib.check(lib.bsr_affine_wgrad(ctypes.byref(cs), dY.data_ptr(), _dt(dY), out.data_ptr(), int(accumulate),
                                     ws.data_ptr(), ws.numel(), _stream(stream)))
     return out
+
+
+def wgrad_multicast(A: BSR, dY: torch.Tensor, mc_ptr: int, prec: str = "fp32", algo: str = "auto",
+                    stream=None) -> None:
+    """Fused a6 + a7 (SURVEY §8f f3 ii): ADD this rank's dW = X_bsr^T . dY into the
+    K x N fp32 buffer behind the multimem (NVLS multicast) address mc_ptr, from the
+    dW kernel itself (multimem.red.add); the NVSwitch sums the ranks.  The caller
+    zeroes the buffer on every rank first and synchronises the ranks afterwards
+    (paper_2311_16883_b200.dist.NvlsGradient)."""
+    lib = _lib.load()
+    dY = _cuda2d(dY, "dY")
+    if dY.shape[0] != A.M:
+        raise ValueError(f"dY has {dY.shape[0]} rows, BSR has M={A.M}")
+    N = dY.shape[1]
+    p = PREC[prec]
+    ws_bytes = lib.bsr_wgrad_workspace_bytes(A.M, A.K, A.b, N, p)
+    ws = workspace(ws_bytes, dY.device, stream=stream) if ws_bytes else None
+    cs = A.c_struct()
+    _lib.check(lib.bsr_wgrad_multicast(ctypes.byref(cs), dY.data_ptr(), _dt(dY), N, ctypes.c_void_p(mc_ptr), p,
+                                       ALGO[algo], ws.data_ptr() if ws is not None else None,
+                                       ws.numel() if ws is not None else 0, _stream(stream)))
 
 
 def set_pdl(mask: int) -> int:

@@ -499,6 +499,34 @@ bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t
     return bsr_wgrad_algo(A, dY, dy_dtype, N, dW, accumulate, prec, BSR_ALGO_AUTO, ws, ws_bytes, stream);
 }
 
+bsr_status_t bsr_wgrad_multicast(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *mc_dW,
+                                 int32_t prec, int32_t algo, void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_bsr(A);
+    if (st != BSR_OK) return st;
+    const int esy = elem_size(dy_dtype);
+    if (esy == 0) return fail(BSR_ERR_INVALID_ARG, "dy_dtype %d is not BSR_DT_F32 or BSR_DT_BF16", dy_dtype);
+    if (N <= 0 || N > (int64_t(1) << 30)) return fail(BSR_ERR_SHAPE, "N=%lld out of range", (long long)N);
+    if (!dY || !mc_dW) return fail(BSR_ERR_INVALID_ARG, "dY or mc_dW is NULL");
+    if (!aligned16(dY) || !aligned16(mc_dW)) return fail(BSR_ERR_ALIGNMENT, "dY or mc_dW is not 16-byte aligned");
+    if (algo != BSR_ALGO_AUTO && algo != BSR_ALGO_TC_RUNS)
+        return fail(BSR_ERR_UNSUPPORTED, "the fused multicast dW exists in the per-run tensor-core kernel only");
+    int kind = -1;
+    if (prec == BSR_PREC_FP32 && A->dtype == BSR_DT_F32 && dy_dtype == BSR_DT_F32) kind = 2;
+    if (prec == BSR_PREC_TF32 && A->dtype == BSR_DT_F32 && dy_dtype == BSR_DT_F32) kind = 0;
+    if (prec == BSR_PREC_BF16 && A->dtype == BSR_DT_BF16 && dy_dtype == BSR_DT_BF16) kind = 1;
+    if (kind < 0 || !bsrp::wgrad_tc_supported(kind, BSR_ALGO_TC_RUNS, A->b, A->K, N) || (kind == 0 && A->b < 32) ||
+        A->b < 16 || N % 128 != 0 || A->K / A->b >= 65536)
+        return fail(BSR_ERR_UNSUPPORTED, "no per-run tensor-core kernel for prec %d, b=%d, N=%lld with these dtypes", prec,
+                    A->b, (long long)N);
+    const size_t need = kind == 2 ? bsrp::wgrad_x3_ws_bytes(A->M, A->K, A->b, N) : bsrp::wgrad_tc_ws_bytes(A->M, A->K, A->b, N);
+    if (need && (!ws || ws_bytes < need))
+        return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+    if (need && !aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
+    return cuda_status(bsrp::launch_wgrad_tc(A->rowptr, A->colidx, A->values, A->nnzb, kind, BSR_ALGO_TC_RUNS, A->M,
+                                             A->K, A->b, dY, N, nullptr, 1, ws, static_cast<cudaStream_t>(stream), mc_dW),
+                       "bsr_wgrad_multicast launch");
+}
+
 uint32_t bsr_set_pdl(uint32_t mask) { return bsrp::g_pdl.exchange(mask); }
 
 /* ---- block-sparse affine layer (affine.cu) ---- */

@@ -98,7 +98,8 @@ size_t wgrad_x3_ws_bytes(int64_t M, int64_t K, int b, int64_t N);
 bool wgrad_tc_supported(int kind, int algo, int b, int64_t K, int64_t N);
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values,
                             int64_t nnzb, int kind, int algo, int64_t M, int64_t K, int b, const void *dY,
-                            int64_t N, float *dW, int accumulate, void *ws, cudaStream_t stream);
+                            int64_t N, float *dW, int accumulate, void *ws, cudaStream_t stream,
+                            float *mc = nullptr);
 
 // Span kernel (wgrad_span.cu): dense-padded per-row spans, CTA-pair MMAs.
 size_t wgrad_span_ws_bytes(int64_t M, int64_t K, int b, int64_t N);

@@ -489,7 +489,10 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_kernel(Prun
 //                       counts the (above, tie) keys before its own flat range
 //                       from shared memory, then scans and packs its range as
 //                       prune_kernel does.  No grid barrier.
-constexpr int64_t kSmallN = 40960;  // keys held in shared memory by every finishing CTA (160 KB)
+constexpr int64_t kSmallN = 24576;  // keys held in shared memory by every finishing CTA (96 KB); measured:
+                                    // at 37632 keys (S12 fc1 b = 16) the per-CTA passes cost more than the
+                                    // cooperative kernel's barriers
+constexpr int kSmallCand = 4096;    // boundary-bin candidates (key, flat index) in shared memory (32 KB)
 
 template <int ES, int B>
 __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_sums_kernel(PruneParams p) {
@@ -522,7 +525,7 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_sums_kernel
 
 template <int ES, int B>
 __global__ void __launch_bounds__(kThreads, 1) prune_finish_kernel(PruneParams p) {
-    extern __shared__ uint32_t s_key[];  // [N] key bits, flat order
+    extern __shared__ uint32_t s_key[];  // [N] key bits, flat order; then the candidate list
     __shared__ uint32_t s_h2[1024];
     __shared__ uint64_t s_warp[32];
     __shared__ uint32_t s_sel[4];
@@ -535,6 +538,8 @@ __global__ void __launch_bounds__(kThreads, 1) prune_finish_kernel(PruneParams p
     };
     const int64_t f0 = flat_start(u0), f1 = flat_start(u1);
     const int N = (int)p.N;
+    uint32_t *s_ck = s_key + ((N + 3) & ~3);  // [kSmallCand] candidate keys
+    uint32_t *s_cf = s_ck + kSmallCand;       // [kSmallCand] their flat indices
     pdl_wait();  // the sums kernel has completed: sumsq and hist1 are final
     // boundary bin of the first digit from the global histogram
     const uint32_t k = (uint32_t)p.k;
@@ -568,18 +573,48 @@ __global__ void __launch_bounds__(kThreads, 1) prune_finish_kernel(PruneParams p
         for (int i = threadIdx.x; i < kH1; i += kThreads) p.hist1[i] = 0;
         if (threadIdx.x == 0) p.bar[32] = 0;
     }
-    // refine the boundary bin over the keys in shared memory: bits 18..9, then 8..0
+    // Refine the boundary bin (bits 18..9, then 8..0).  Its keys are first compacted
+    // into a candidate list (key, flat index) in shared memory, so the two
+    // histogram passes and the prefix count run over the candidates only; a bin
+    // too large for the list (heavy ties) is refined over all keys instead.
+    const uint32_t prefix1 = prefix;
     int shift = 19;
     uint32_t r = k - above;
+    uint32_t nc = 0;
+    const bool refine = r < bincnt;
+    const bool use_cand = refine && bincnt <= (uint32_t)kSmallCand;
+    if (use_cand) {
+        __syncthreads();  // every thread has read the clean-up flag in s_sel[3]
+        if (threadIdx.x == 0) s_sel[3] = 0;
+        __syncthreads();
+        for (int fb = 0; fb < N; fb += kThreads) {
+            const int f = fb + threadIdx.x;
+            const bool in = f < N && (s_key[f] >> 19) == prefix1;
+            const uint32_t m = __ballot_sync(0xffffffffu, in);
+            uint32_t base = 0;
+            if (m && lane == 0) base = atomicAdd(&s_sel[3], (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (in) {
+                const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+                s_ck[pos] = s_key[f];
+                s_cf[pos] = (uint32_t)f;
+            }
+        }
+        __syncthreads();
+        nc = s_sel[3];  // == bincnt
+        __syncthreads();
+    }
+    const uint32_t *arr = use_cand ? s_ck : s_key;
+    const int len = use_cand ? (int)nc : N;
     for (int pass = 0; pass < 2 && r < bincnt; ++pass) {
         const int w = pass == 0 ? 10 : 9;
         const int nshift = shift - w;
         for (int i = threadIdx.x; i < (1 << w); i += kThreads) s_h2[i] = 0;
         __syncthreads();
-        for (int fb = 0; fb < N; fb += kThreads) {
+        for (int fb = 0; fb < len; fb += kThreads) {
             const int f = fb + threadIdx.x;
-            const uint32_t key = f < N ? s_key[f] : 0u;
-            const bool in = f < N && (key >> shift) == prefix;
+            const uint32_t key = f < len ? arr[f] : 0u;
+            const bool in = f < len && (key >> shift) == prefix;
             const uint32_t bin = (key >> nshift) & ((1u << w) - 1u);
             const uint32_t im = __ballot_sync(0xffffffffu, in);
             if (!im) continue;
@@ -599,12 +634,23 @@ __global__ void __launch_bounds__(kThreads, 1) prune_finish_kernel(PruneParams p
         shift = nshift;
         r = k - above;
     }
-    // (above, tie) counts of every block before this CTA's range
+    // (above, tie) counts of every block before this CTA's range: keys above the
+    // first-digit bin from all keys, the rest from the candidates (or all keys)
     uint32_t na = 0, nt = 0;
-    for (int64_t f = threadIdx.x; f < f0; f += kThreads) {
-        const uint32_t kk = s_key[f] >> shift;
-        na += kk > prefix;
-        nt += kk == prefix;
+    if (use_cand) {
+        for (int64_t f = threadIdx.x; f < f0; f += kThreads) na += (s_key[f] >> 19) > prefix1;
+        for (uint32_t i = threadIdx.x; i < nc; i += kThreads) {
+            if ((int64_t)s_cf[i] >= f0) continue;
+            const uint32_t kk = s_ck[i] >> shift;
+            na += kk > prefix;
+            nt += kk == prefix;
+        }
+    } else {
+        for (int64_t f = threadIdx.x; f < f0; f += kThreads) {
+            const uint32_t kk = s_key[f] >> shift;
+            na += kk > prefix;
+            nt += kk == prefix;
+        }
     }
     uint64_t pre;
     block_excl_scan(((uint64_t)na << 32) | nt, s_warp, pre);
@@ -909,7 +955,7 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
     // (no per-launch memset: the kernels leave their workspace header zeroed, see above)
     cudaError_t e = cudaSuccess;
     if (p.N <= kSmallN) {
-        const size_t smem = (size_t)((p.N + 3) & ~int64_t(3)) * 4;
+        const size_t smem = (size_t)((p.N + 3) & ~int64_t(3)) * 4 + (size_t)kSmallCand * 8;
         e = cudaFuncSetAttribute(prune_finish_kernel<ES, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         const int64_t per = kThreads / 32;  // one unit per warp

@@ -263,9 +263,11 @@ struct Params {
     const int32_t *rowptr, *colidx;
     const uint8_t *values;
     float *dW, *ws;
+    float *mc;                   // multimem (NVLS multicast) address of the summed dW, or null
     int64_t nbr, N, K;
     int nkr, nsplit, kr_blocks;  // kcol range = kr_blocks blocks
-    int nbslots, na, mode;       // B-ring block slots, TMEM A buffers; mode: 0 store, 1 reduce-add, 3 partial -> ws[split]
+    int nbslots, na, mode;       // B-ring block slots, TMEM A buffers; mode: 0 store, 1 reduce-add, 3 partial -> ws[split],
+                                 // 4 multimem reduce-add into p.mc (NVLS; one split)
     int chunk_steps;             // steps of one metadata chunk (rowptr + colidx staged in smem)
     int sa;                      // shared-memory A ring stages
     uint32_t a_col0;             // first TMEM column of the A buffers
@@ -914,6 +916,23 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
             uint32_t v[32];
             TMEM_LD16(tmem + lane_base + c, v);
             TMEM_LD16(tmem + lane_base + c + 16, (v + 16));
+            if (p.mode == 4) {  // fused all-reduce: add this tile into the multicast dW (NVSwitch reduction)
+                uint32_t w[32];
+                if constexpr (C::X3) {
+                    TMEM_LD16(tmem + lane_base + p.corr_col + c, w);
+                    TMEM_LD16(tmem + lane_base + p.corr_col + c + 16, (w + 16));
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int nrow = min(32, ncols - c);
+                float *dst = p.mc + (int64_t)(row0 + c) * p.N + n0 + ew * 32 + lane;
+                for (int i = 0; i < nrow; ++i) {
+                    float x = __uint_as_float(v[i]);
+                    if constexpr (C::X3) x = __fadd_rn(x, __uint_as_float(w[i]));
+                    asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(dst + (int64_t)i * p.N), "f"(x)
+                                 : "memory");
+                }
+                continue;
+            }
             if constexpr (C::X3) {  // D = D_main + D_corr, one round-to-nearest fp32 add
                 uint32_t w[32];
                 TMEM_LD16(tmem + lane_base + p.corr_col + c, w);
@@ -962,7 +981,8 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
 // of the (ordered) adds so the L2-resident partials stream at full rate.  <= 64
 // registers: 4 CTAs per SM, so the C2 grid (576 CTAs) runs in one wave.
 __global__ void __launch_bounds__(256, 4) splitk_reduce_kernel(const float4 *__restrict__ ws, float4 *__restrict__ dW,
-                                                               int64_t n4, int nsplit, int accumulate, int trig) {
+                                                               int64_t n4, int nsplit, int accumulate, int trig,
+                                                               float4 *__restrict__ mc) {
     if (trig) pdl_trigger();
     pdl_wait();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
@@ -978,7 +998,12 @@ __global__ void __launch_bounds__(256, 4) splitk_reduce_kernel(const float4 *__r
                     a.x += v[u].x; a.y += v[u].y; a.z += v[u].z; a.w += v[u].w;
                 }
         }
-        dW[i] = a;
+        if (mc)  // fused all-reduce: the split sum is added into the multicast dW (NVSwitch reduction)
+            asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc + i), "f"(a.x),
+                         "f"(a.y), "f"(a.z), "f"(a.w)
+                         : "memory");
+        else
+            dW[i] = a;
     }
 }
 
@@ -1062,7 +1087,7 @@ static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms) {
 template <int KIND, int B>
 static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
                             int64_t M, int64_t K, const void *dY, int64_t N, float *dW, int accumulate,
-                            float *ws, cudaStream_t stream) {
+                            float *ws, cudaStream_t stream, float *mc) {
     using C = Cfg<KIND, B>;
     int dev = 0, sms = kSplitSMs;
     cudaGetDevice(&dev);
@@ -1116,7 +1141,8 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     p.corr_col = pl.corr_col;
     p.chunk_steps = pl.chunk_steps;
     p.ws = ws;
-    p.mode = pl.nsplit > 1 ? 3 : accumulate ? 1 : 0;
+    p.mc = mc;
+    p.mode = pl.nsplit > 1 ? 3 : mc ? 4 : accumulate ? 1 : 0;
     p.pdl_trig = (pdl_flags() & 2) ? 1 : (pdl_flags() & 4) ? 2 : 0;
     auto kern = wgrad_tc_kernel<KIND, B>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
@@ -1130,7 +1156,8 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     const int64_t n4 = K * N / 4;
     const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 4));
     e = launch_pdl(pdl_flags() & 32, splitk_reduce_kernel, dim3(rgrid), dim3(256), 0, stream, reinterpret_cast<const float4 *>(ws),
-                   reinterpret_cast<float4 *>(dW), n4, (int)pl.nsplit, accumulate, (pdl_flags() & 8) ? 1 : 0);
+                   reinterpret_cast<float4 *>(dW), n4, (int)pl.nsplit, mc ? 0 : accumulate, (pdl_flags() & 8) ? 1 : 0,
+                   reinterpret_cast<float4 *>(mc));
     count_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -1145,7 +1172,7 @@ cudaError_t launch_splitk_reduce(const float *ws, float *dW, int64_t n, int nspl
     const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 4));
     cudaError_t e = launch_pdl(pdl_flags() & 32, tc::splitk_reduce_kernel, dim3(rgrid), dim3(256), 0, stream,
                                reinterpret_cast<const float4 *>(ws), reinterpret_cast<float4 *>(dW), n4, nsplit,
-                               accumulate, (pdl_flags() & 8) ? 1 : 0);
+                               accumulate, (pdl_flags() & 8) ? 1 : 0, static_cast<float4 *>(nullptr));
     count_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -1207,15 +1234,16 @@ bool wgrad_tc_supported(int kind, int algo, int b, int64_t K, int64_t N) {
 
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
                             int kind, int algo, int64_t M, int64_t K, int b, const void *dY, int64_t N, float *dW,
-                            int accumulate, void *ws, cudaStream_t stream) {
+                            int accumulate, void *ws, cudaStream_t stream, float *mc) {
+    if (mc && !use_runs_kernel(kind, algo, b, K)) return cudaErrorNotSupported;  // multicast: per-run kernel only
     if (!use_runs_kernel(kind, algo, b, K))
         return launch_wgrad_span(rowptr, colidx, values, nnzb, kind, M, K, b, dY, N, dW, accumulate, ws, stream);
-    if (!values || nnzb == 0) {  // no stored block: dW = 0 (or unchanged)
-        return accumulate ? cudaSuccess : cudaMemsetAsync(dW, 0, (size_t)K * N * sizeof(float), stream);
+    if (!values || nnzb == 0) {  // no stored block: dW = 0 (or unchanged; nothing to add into the multicast dW)
+        return accumulate || mc ? cudaSuccess : cudaMemsetAsync(dW, 0, (size_t)K * N * sizeof(float), stream);
     }
 #define TC_CASE(KD, B_) \
     if (kind == KD && b == B_) return tc::launch_t<KD, B_>(rowptr, colidx, values, nnzb, M, K, dY, N, dW, accumulate, \
-                                                            static_cast<float *>(ws), stream);
+                                                            static_cast<float *>(ws), stream, mc);
     TC_CASE(0, 32) TC_CASE(0, 64) TC_CASE(1, 16) TC_CASE(1, 32) TC_CASE(1, 64) TC_CASE(2, 32) TC_CASE(2, 64)
 #undef TC_CASE
     return cudaErrorInvalidValue;

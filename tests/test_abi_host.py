@@ -187,3 +187,13 @@ def test_wgrad_algo_set_pdl_and_affine_validation(lib):
     assert lib.bsr_affine_wgrad(ctypes.byref(good), FAKE, 0, W, 3, WS, BIG, None) == 1             # accumulate
     assert lib.bsr_affine_wgrad(ctypes.byref(good), FAKE + 4, 0, W, 0, WS, BIG, None) == 4         # alignment
     assert lib.bsr_affine_wgrad(ctypes.byref(good), FAKE, 0, W, 0, WS, 16, None) == 5             # workspace
+
+
+def test_wgrad_multicast_validation(lib):
+    good = _lib.BsrT(256, 256, 16, 0, 10, FAKE, FAKE, FAKE)
+    MC, WS, BIG = FAKE + 0x1000000, FAKE + 0x800000, 1 << 30
+    assert lib.bsr_wgrad_multicast(ctypes.byref(good), FAKE, 0, 256, None, 0, 0, WS, BIG, None) == 1       # mc
+    assert lib.bsr_wgrad_multicast(ctypes.byref(good), FAKE, 0, 256, MC, 0, 2, WS, BIG, None) == 3         # span
+    assert lib.bsr_wgrad_multicast(ctypes.byref(good), FAKE, 0, 256, MC, 1, 0, WS, BIG, None) == 3         # tf32 b=16
+    assert lib.bsr_wgrad_multicast(ctypes.byref(good), FAKE, 0, 256, MC, 2, 0, WS, BIG, None) == 3         # bf16 + f32 X
+    assert lib.bsr_wgrad_multicast(ctypes.byref(good), FAKE + 4, 0, 256, MC, 0, 0, WS, BIG, None) == 4     # align

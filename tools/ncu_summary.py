@@ -65,11 +65,13 @@ def summarise(outdir, pairs):
         name = key.replace("|", "_")
         with open(os.path.join(outdir, f"{name}.json"), "w") as f:
             json.dump({"report": os.path.basename(rep), "key": key, "launches": launches}, f, indent=1)
-        L = launches[0]
-        dram = to_bytes(L["dram__bytes_read.sum"]) + to_bytes(L["dram__bytes_write.sum"])
-        traffic[key] = {"dram_bytes_per_launch": dram, "kernel": L["kernel"],
-                        "ncu_duration": L.get("gpu__time_duration.sum"), "source": f"{outdir}/{name}.json"}
-        print(key, L["kernel"], L.get("gpu__time_duration.sum"), f"dram {dram / 1e6:.1f} MB")
+        # a phase may be several kernels (prune: sums + finish; dW: tensor-core kernel + split-K
+        # reduce): the report holds one launch of each, and the phase's traffic is their sum
+        dram = sum(to_bytes(L["dram__bytes_read.sum"]) + to_bytes(L["dram__bytes_write.sum"]) for L in launches)
+        traffic[key] = {"dram_bytes_per_launch": dram, "kernel": " + ".join(L["kernel"] for L in launches),
+                        "ncu_duration": " + ".join(str(L.get("gpu__time_duration.sum")) for L in launches),
+                        "source": f"{outdir}/{name}.json"}
+        print(key, traffic[key]["kernel"][:120], traffic[key]["ncu_duration"], f"dram {dram / 1e6:.1f} MB")
     with open(tpath, "w") as f:
         json.dump(traffic, f, indent=1, sort_keys=True)
 
