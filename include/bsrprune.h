@@ -311,6 +311,18 @@ BSR_API bsr_status_t bsr_prune_rows(const void *X, int64_t M, int64_t K, int32_t
 BSR_API bsr_status_t bsr_decompress_rows(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t M,
                                          int64_t K, int32_t b, int32_t dtype, void *X_out, void *stream);
 BSR_API size_t bsr_wgrad_rows_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N);
+/* The same dW on the tensor cores: with per-sample 1 x b segments an 8-row tensor-core
+ * K step almost never meets a fully pruned b-wide tile (0.5^8 at keep 0.5), so the
+ * kept rows are rebuilt densely (zeros elsewhere), viewed as a keep-all 32 x 32 BSR
+ * and contracted by the per-run tcgen05 kernel: FP32 grade (3xTF32, rel-F <= 1e-5)
+ * for f32 X and dY, bf16 for bf16 X and dY.  Needs 32 | M, 32 | K, N % 128 == 0,
+ * dY in X's dtype (else BSR_ERR_UNSUPPORTED); workspace from the query (0 if the
+ * shape is not supported). */
+BSR_API size_t bsr_wgrad_rows_tc_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t x_dtype);
+BSR_API bsr_status_t bsr_wgrad_rows_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnz,
+                                       int64_t M, int64_t K, int32_t b, int32_t x_dtype, const void *dY,
+                                       int32_t dy_dtype, int64_t N, float *dW, int32_t accumulate, void *ws,
+                                       size_t ws_bytes, void *stream);
 BSR_API bsr_status_t bsr_wgrad_rows(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnz,
                                     int64_t M, int64_t K, int32_t b, int32_t x_dtype, const void *dY,
                                     int32_t dy_dtype, int64_t N, float *dW, int32_t accumulate, void *ws,

@@ -395,6 +395,70 @@ bsr_status_t bsr_wgrad_rows(const int32_t *rowptr, const int32_t *colidx, const 
                        "bsr_wgrad_rows launch");
 }
 
+/* 1 x b variant on the tensor cores: rebuild the masked rows densely, view them as a
+ * keep-all 32 x 32 BSR and run the per-run tcgen05 kernel (FP32 grade for f32,
+ * bf16 for bf16).  Workspace layout: [masked X: M*K elems][32x32 values: M*K elems]
+ * [rowptr: M/32+1][colidx: (M/32)(K/32)][tensor-core split-K partials]. */
+namespace {
+constexpr int kRowsTcB = 32;
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+struct RowsTcWs {
+    size_t xm, vals, rp, ci, tc, total;
+};
+RowsTcWs rows_tc_layout(int64_t M, int64_t K, int64_t N, int es) {
+    RowsTcWs w{};
+    const int64_t nb = (M / kRowsTcB) * (K / kRowsTcB);
+    size_t o = 0;
+    w.xm = o;   o += align256((size_t)M * K * es);
+    w.vals = o; o += align256((size_t)M * K * es);
+    w.rp = o;   o += align256((size_t)(M / kRowsTcB + 1) * 4);
+    w.ci = o;   o += align256((size_t)nb * 4);
+    w.tc = o;
+    o += align256(es == 4 ? bsrp::wgrad_x3_ws_bytes(M, K, kRowsTcB, N) : bsrp::wgrad_tc_ws_bytes(M, K, kRowsTcB, N));
+    w.total = o;
+    return w;
+}
+}  // namespace
+
+size_t bsr_wgrad_rows_tc_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t x_dtype) {
+    if (M <= 0 || K <= 0 || N <= 0 || !supported_b(b) || K % b || elem_size(x_dtype) == 0) return 0;
+    if (M % kRowsTcB || K % kRowsTcB || N % 128) return 0;
+    return rows_tc_layout(M, K, N, elem_size(x_dtype)).total;
+}
+
+bsr_status_t bsr_wgrad_rows_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnz, int64_t M,
+                               int64_t K, int32_t b, int32_t x_dtype, const void *dY, int32_t dy_dtype, int64_t N,
+                               float *dW, int32_t accumulate, void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_rows(M, K, b, x_dtype);
+    if (st != BSR_OK) return st;
+    if (dy_dtype != x_dtype) return fail(BSR_ERR_UNSUPPORTED, "tensor-core 1 x b dW needs dY in the dtype of X");
+    if (M % kRowsTcB || K % kRowsTcB)
+        return fail(BSR_ERR_UNSUPPORTED, "tensor-core 1 x b dW needs 32 | M and 32 | K (M=%lld, K=%lld)", (long long)M,
+                    (long long)K);
+    if (N <= 0 || N % 128) return fail(BSR_ERR_UNSUPPORTED, "tensor-core 1 x b dW needs N %% 128 == 0 (N=%lld)", (long long)N);
+    if (!rowptr || !dY || !dW) return fail(BSR_ERR_INVALID_ARG, "rowptr, dY or dW is NULL");
+    if (nnz > 0 && (!colidx || !values)) return fail(BSR_ERR_INVALID_ARG, "colidx / values are NULL with nnz > 0");
+    if (accumulate != 0 && accumulate != 1) return fail(BSR_ERR_INVALID_ARG, "accumulate must be 0 or 1");
+    if (!aligned16(dY) || !aligned16(dW)) return fail(BSR_ERR_ALIGNMENT, "dY or dW is not 16-byte aligned");
+    const int es = elem_size(x_dtype);
+    const RowsTcWs w = rows_tc_layout(M, K, N, es);
+    if (!ws || ws_bytes < w.total)
+        return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, w.total);
+    if (!aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
+    char *base = static_cast<char *>(ws);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    void *xm = base + w.xm;
+    cudaError_t e = bsrp::launch_decompress_rows(rowptr, colidx, nnz > 0 ? values : nullptr, M, K, b, es, xm, s);
+    if (e != cudaSuccess) return cuda_status(e, "bsr_wgrad_rows_tc (masked rows)");
+    const int64_t nbk = (M / kRowsTcB) * (K / kRowsTcB);
+    int32_t *rp = reinterpret_cast<int32_t *>(base + w.rp), *ci = reinterpret_cast<int32_t *>(base + w.ci);
+    e = bsrp::launch_prune(xm, M, K, kRowsTcB, es, nbk, rp, ci, base + w.vals, nullptr, s);  // k = N: one copy pass
+    if (e != cudaSuccess) return cuda_status(e, "bsr_wgrad_rows_tc (dense blocks)");
+    return cuda_status(bsrp::launch_wgrad_tc(rp, ci, base + w.vals, nbk, es == 4 ? 2 : 1, BSR_ALGO_TC_RUNS, M, K, kRowsTcB,
+                                             dY, N, dW, accumulate, base + w.tc, s),
+                       "bsr_wgrad_rows_tc launch");
+}
+
 /* ---- producer fusion ---- */
 bsr_status_t bsr_act_block_sumsq(const void *Z, void *X_out, int64_t M, int64_t K, int32_t b, int32_t dtype,
                                  int32_t act, void *ws, size_t ws_bytes, void *stream) {

@@ -61,14 +61,27 @@ def decompress_rows(A: RowBSR, out: torch.Tensor | None = None, stream=None) -> 
 
 
 def wgrad_rows(A: RowBSR, dY: torch.Tensor, out: torch.Tensor | None = None, accumulate: bool = False,
-               stream=None) -> torch.Tensor:
-    """dW = X_bsr^T . dY (K x N fp32) over the kept segments, fp32 FFMA (deterministic)."""
+               stream=None, tensor_cores: bool | None = None) -> torch.Tensor:
+    """dW = X_bsr^T . dY (K x N fp32) over the kept segments.  FP32 FFMA
+    (deterministic), or -- tensor_cores=True, or None when the shape allows it --
+    the tcgen05 kernel on the densely rebuilt kept rows (FP32 grade for f32, bf16
+    for bf16 storage; include/bsrprune.h bsr_wgrad_rows_tc)."""
     lib = _lib.load()
     N = dY.shape[1]
     if dY.shape[0] != A.M:
         raise ValueError(f"dY has {dY.shape[0]} rows, the BSR has M={A.M}")
     if out is None:
         out = torch.empty(A.K, N, dtype=torch.float32, device=dY.device)
+    tc_ws = lib.bsr_wgrad_rows_tc_workspace_bytes(A.M, A.K, A.b, N, _dt(A.values))
+    if tensor_cores is None:
+        tensor_cores = bool(tc_ws) and dY.dtype == A.values.dtype
+    if tensor_cores:
+        ws = workspace(tc_ws, dY.device, kind="rows_tc", stream=stream)
+        _lib.check(lib.bsr_wgrad_rows_tc(A.rowptr.data_ptr(), A.colidx.data_ptr() if A.nnz else None,
+                                         A.values.data_ptr() if A.nnz else None, A.nnz, A.M, A.K, A.b, _dt(A.values),
+                                         dY.data_ptr(), _dt(dY), N, out.data_ptr(), int(accumulate), ws.data_ptr(),
+                                         ws.numel(), _stream(stream)))
+        return out
     ws_bytes = lib.bsr_wgrad_rows_workspace_bytes(A.M, A.K, A.b, N)
     ws = workspace(ws_bytes, dY.device, stream=stream) if ws_bytes else None
     _lib.check(lib.bsr_wgrad_rows(A.rowptr.data_ptr(), A.colidx.data_ptr() if A.nnz else None,

@@ -84,9 +84,11 @@ def timed(fn, sets, reps):
 
 
 def prec_for(dtype, b):
+    """bf16 storage: the bf16 tensor cores where they exist; fp32 storage: the FP32
+    grade (3xTF32 tensor cores at b >= 32, FFMA below) -- the library's defaults."""
     if dtype == torch.bfloat16:
         return "bf16" if b >= 16 else "fp32"
-    return "tf32" if b >= 16 else "fp32"
+    return "fp32"
 
 
 def sweep_c3(out, hbm, bf16_tf, nsets=3, reps=6):
@@ -116,7 +118,8 @@ def sweep_c3(out, hbm, bf16_tf, nsets=3, reps=6):
                     wb = metrics.wgrad_bytes(M, K, b, k, N, s, s, r_ne)
                     wf = metrics.wgrad_flops(b, k, N)
                     db = metrics.decompress_bytes(M, K, b, k, s)
-                    tc_peak = bf16_tf if prec == "bf16" else bf16_tf / 2 if prec == "tf32" else None
+                    tc_peak = bf16_tf if prec == "bf16" else bf16_tf / 2 if prec == "tf32" else (
+                        bf16_tf / 6 if b >= 32 else None)  # FP32 grade: 3xTF32 (useful flops) or FFMA
                     w_tf = wf / (t_w * 1e-3) / 1e12
                     w_gbs = wb / (t_w * 1e-3) / 1e9
                     roof_t = max(wb / (hbm * 1e9), wf / (tc_peak * 1e12) if tc_peak else 0.0)
