@@ -136,3 +136,27 @@ def test_rows_select_keys_at_shared_memory_limit(S, K, b):
     np.testing.assert_array_equal(A.rowptr.cpu().numpy(), ref["rowptr"])
     np.testing.assert_array_equal(A.colidx.cpu().numpy(), ref["colidx"])
     np.testing.assert_array_equal(A.values.cpu().numpy().view(np.int32), ref["values"].reshape(-1, b).view(np.int32))
+
+
+@pytest.mark.parametrize("bf16", [False, True])
+@pytest.mark.parametrize("keep", [0.1, 0.5, 1.0])
+def test_wgrad_rows_tensor_cores(bf16, keep):
+    """The 1 x b variant's dW on the tensor cores (kept rows rebuilt densely, keep-all
+    32 x 32 BSR, per-run tcgen05 kernel: FP32 grade for f32, bf16 for bf16) against
+    the oracle on the GPU's own selection, and against the FFMA kernel."""
+    S, nsamp, K, N, b = 196, 4, 384, 256, 16
+    M = S * nsamp
+    X = synth.f_aff(M, K, 55)
+    dY = synth.grad_out(M, N, 55)
+    if bf16:
+        X, dY = synth.to_bf16_bits(X), synth.to_bf16_bits(dY)
+    A = bp.prune_rows(to_torch(X, bf16=bf16), b, keep, sample_rows=S)
+    torch.cuda.synchronize()
+    v = A.values.cpu()
+    vals = (synth.bf16_bits_to_f32(v.view(torch.int16).numpy()) if bf16 else v.numpy()).reshape(-1, 1, b)
+    want = oracle.wgrad_rect(A.rowptr.cpu().numpy(), A.colidx.cpu().numpy(), vals, M, K, 1, b,
+                             synth.bf16_bits_to_f32(dY) if bf16 else dY)
+    tc = bp.wgrad_rows(A, to_torch(dY, bf16=bf16), tensor_cores=True).cpu().numpy()
+    ff = bp.wgrad_rows(A, to_torch(dY, bf16=bf16), tensor_cores=False).cpu().numpy()
+    assert oracle.rel_frobenius(tc, want) <= 1e-5
+    assert oracle.rel_frobenius(ff, want) <= 1e-5
