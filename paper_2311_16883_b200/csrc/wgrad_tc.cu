@@ -326,11 +326,19 @@ struct Cfg {
     static constexpr int ISSUERS = X3 ? 4 : 2;
     static constexpr int SPLITTERS = X3 ? 4 : 0;            // warps splitting landed B blocks into hi / lo
     // warps: 0 B producer, 1-2 MMA, 3 planner, 4-7 A movers (even steps) + epilogue,
-    // 8 A producer, 9-12 A movers (odd steps), then extra MMA issuers, then splitters
+    // 8 A producer, 9-12 A movers (odd steps); FP32 grade: 13-14 splitters, 15-16 MMA,
+    // 17-18 splitters -- the four MMA warps sit on the four SM sub-partitions (warp % 4 =
+    // 1, 2, 3, 0), as in the issue-rate micro-benchmark (at C2 the placement measured
+    // the same as warps 1, 2, 13, 14: the per-step pipeline, not the issue slot, paces it)
     static constexpr int WARPS = 13 + (ISSUERS - 2) + SPLITTERS;
     static constexpr int THREADS = 32 * WARPS;
-    static constexpr int SPLIT_W0 = 13 + (ISSUERS - 2);     // first splitter warp
     static constexpr int BAR1_THREADS = 32 * (8 + ISSUERS);  // issuers + A movers (accumulator zeroed)
+    __device__ static constexpr int issuer(int w) {          // MMA issuer index of warp w, or -1
+        return w == 1 ? 0 : w == 2 ? 1 : (X3 && w == 15) ? 2 : (X3 && w == 16) ? 3 : -1;
+    }
+    __device__ static constexpr int splitter(int w) {        // splitter index of warp w, or -1
+        return !X3 ? -1 : w == 13 ? 0 : w == 14 ? 1 : w == 17 ? 2 : w == 18 ? 3 : -1;
+    }
 };
 
 // This thread's dY column of the step's slab in shared memory (row-major, 128
@@ -685,7 +693,7 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
                 }
             }
         }
-    } else if (warp == 1 || warp == 2 || (warp >= 13 && warp < C::SPLIT_W0)) {
+    } else if (C::issuer(warp) >= 0) {
         // ------------------------------------------------ MMA issuers (whole warps, one elected lane issues)
         // Issuer i (warps 1, 2, then 13.. for the FP32 grade) issues the runs in
         // accumulator blocks [jb(i), jb(i + 1)): a warp issues one tcgen05.mma per
@@ -698,7 +706,7 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
         tc_fence_before();
         asm volatile("bar.sync 1, %0;" ::"r"(C::BAR1_THREADS) : "memory");  // accumulator zeroed by warps 4-7
         tc_fence_after();
-        const int iw = warp <= 2 ? warp - 1 : warp - 11;
+        const int iw = C::issuer(warp);
         const uint32_t col_lo = (uint32_t)(jb(iw) * B), col_hi = (uint32_t)(jb(iw + 1) * B);
         // warp-uniform copies (REDUX results live in uniform registers)
         const uint32_t tmem_u = __reduce_or_sync(0xffffffffu, tmem);
@@ -761,7 +769,7 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
             if (lane == 0) mbar_arrive(plan_empty + buf);  // this chunk's plan is no longer read
         }
         if (lane == 0) tc_commit(accfull);
-    } else if (C::X3 && warp >= C::SPLIT_W0) {
+    } else if (C::X3 && C::splitter(warp) >= 0) {
         // ------------------------------------------------ B splitters (FP32 grade)
         // Walk the B producer's step sequence; once a step's blocks have landed
         // (`full`), write lo(x) = x - hi(x) of every value x at the same offset of
@@ -771,7 +779,7 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
         // kind::tf32 reads an fp32 operand as its sign, exponent and top 10
         // mantissa bits, i.e. exactly hi(x) (truncation; writing hi(x) explicitly
         // gave bit-identical dW, R15/R17).
-        const int sw = warp - C::SPLIT_W0;
+        const int sw = C::splitter(warp);
         int j = 0;
         for (int c = 0; c < nchunks; ++c) {
             const int buf = c & 1;
