@@ -933,7 +933,9 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 const int nrow = min(32, ncols - c);
                 float *dst = p.mc + (int64_t)(row0 + c) * p.N + n0 + ew * 32 + lane;
-                for (int i = 0; i < nrow; ++i) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {  // unrolled: v, w stay in registers
+                    if (i >= nrow) break;
                     float x = __uint_as_float(v[i]);
                     if constexpr (C::X3) x = __fadd_rn(x, __uint_as_float(w[i]));
                     asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(dst + (int64_t)i * p.N), "f"(x)
