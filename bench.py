@@ -383,7 +383,12 @@ def run_native(a):
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator size (nranks) in the log
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-    rank, local, world = D.init("nccl")
+    # BSRP_BENCH_BACKEND=gloo: test hook that runs the N > 1 control flow (barriers, max/sum
+    # over ranks, the dW all-reduce, C4's buckets) with gloo, ranks sharing the visible GPUs
+    backend = os.environ.get("BSRP_BENCH_BACKEND", "nccl")
+    rank, local, world = D.init(backend)
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if a.config == "C4":

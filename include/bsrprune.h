@@ -93,8 +93,16 @@ typedef enum { BSR_PREC_FP32 = 0, BSR_PREC_TF32 = 1, BSR_PREC_BF16 = 2 } bsr_pre
  *             grade b in {32, 64}).
  *   TC_SPAN : CTA-pair span kernel (tf32/bf16, b >= 16; not the FP32 grade).
  *   SIMT    : fp32 FFMA (any b, f32 or bf16 operands; BSR_PREC_FP32 only).
+ *   TC_DENSE: dense rebuild -- the masked X rebuilt in the workspace, viewed as a
+ *             keep-all 32 x 32 BSR and contracted by the per-run kernel (any b; X and
+ *             dY both f32 (FP32 grade / tf32) or both bf16; 32 | M, 32 | K,
+ *             N % 128 == 0).  AUTO takes it below the native tensor-core block sizes
+ *             (FP32 grade b < 32, tf32 / bf16 b < 16): computing the pruned blocks of a
+ *             32 x 32 tile as zeros on the tensor cores beats the FFMA kernel there.
  * A combination the chosen family does not implement is BSR_ERR_UNSUPPORTED. */
-typedef enum { BSR_ALGO_AUTO = 0, BSR_ALGO_TC_RUNS = 1, BSR_ALGO_TC_SPAN = 2, BSR_ALGO_SIMT = 3 } bsr_algo_t;
+typedef enum {
+    BSR_ALGO_AUTO = 0, BSR_ALGO_TC_RUNS = 1, BSR_ALGO_TC_SPAN = 2, BSR_ALGO_SIMT = 3, BSR_ALGO_TC_DENSE = 4
+} bsr_algo_t;
 
 /* A Block Sparse Row matrix.  The struct itself lives in host
  * memory; the three arrays are device memory owned by the caller.

@@ -17,7 +17,7 @@ STATUS_NAMES = {0: "BSR_OK", 1: "BSR_ERR_INVALID_ARG", 2: "BSR_ERR_SHAPE", 3: "B
                 4: "BSR_ERR_ALIGNMENT", 5: "BSR_ERR_WORKSPACE", 6: "BSR_ERR_CUDA"}
 DT_F32, DT_BF16 = 0, 1
 PREC = {"fp32": 0, "tf32": 1, "bf16": 2}
-ALGO = {"auto": 0, "runs": 1, "span": 2, "simt": 3}
+ALGO = {"auto": 0, "runs": 1, "span": 2, "simt": 3, "dense": 4}
 
 EXPORTED = ["bsr_num_blocks", "bsr_keep_count", "bsr_storage_bytes", "bsr_prune_workspace_bytes",
             "bsr_wgrad_workspace_bytes", "bsr_prune", "bsr_prune_k", "bsr_block_sumsq", "bsr_decompress",

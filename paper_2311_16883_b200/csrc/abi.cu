@@ -71,6 +71,43 @@ bsr_status_t check_shape(int64_t M, int64_t K, int32_t b, int32_t dtype) {
     return BSR_OK;
 }
 
+/* Dense rebuild for the tensor cores (block sizes the tcgen05 kernels cannot skip at,
+ * and the 1 x b variant): the masked X is rebuilt densely in the workspace, viewed as a
+ * keep-all 32 x 32 BSR (one copy pass) and contracted by the per-run tcgen05 kernel.
+ * Workspace: [masked X: M*K elems][32x32 values: M*K elems][rowptr][colidx][TC partials]. */
+constexpr int kDenseB = 32;
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+struct DenseTcWs {
+    size_t xm, vals, rp, ci, tc, total;
+};
+bool dense_tc_shape_ok(int64_t M, int64_t K, int64_t N) {
+    return M > 0 && K > 0 && N > 0 && M % kDenseB == 0 && K % kDenseB == 0 && N % 128 == 0 && K / kDenseB < 65536;
+}
+DenseTcWs dense_tc_layout(int64_t M, int64_t K, int64_t N, int es, int kind) {
+    DenseTcWs w{};
+    const int64_t nb = (M / kDenseB) * (K / kDenseB);
+    size_t o = 0;
+    w.xm = o;   o += align256((size_t)M * K * es);
+    w.vals = o; o += align256((size_t)M * K * es);
+    w.rp = o;   o += align256((size_t)(M / kDenseB + 1) * 4);
+    w.ci = o;   o += align256((size_t)nb * 4);
+    w.tc = o;
+    o += align256(kind == 2 ? bsrp::wgrad_x3_ws_bytes(M, K, kDenseB, N) : bsrp::wgrad_tc_ws_bytes(M, K, kDenseB, N));
+    w.total = o;
+    return w;
+}
+// The masked X is in ws at w.xm: re-block it and run the tensor cores.
+cudaError_t dense_tc_finish(int64_t M, int64_t K, int es, int kind, const void *dY, int64_t N, float *dW,
+                            int accumulate, void *ws, const DenseTcWs &w, cudaStream_t s) {
+    char *base = static_cast<char *>(ws);
+    const int64_t nbk = (M / kDenseB) * (K / kDenseB);
+    int32_t *rp = reinterpret_cast<int32_t *>(base + w.rp), *ci = reinterpret_cast<int32_t *>(base + w.ci);
+    cudaError_t e = bsrp::launch_prune(base + w.xm, M, K, kDenseB, es, nbk, rp, ci, base + w.vals, nullptr, s);  // k = N
+    if (e != cudaSuccess) return e;
+    return bsrp::launch_wgrad_tc(rp, ci, base + w.vals, nbk, kind, BSR_ALGO_TC_RUNS, M, K, kDenseB, dY, N, dW, accumulate,
+                                 base + w.tc, s);
+}
+
 bsr_status_t check_bsr(const bsr_t *A) {
     if (!A) return fail(BSR_ERR_INVALID_ARG, "BSR descriptor is NULL");
     bsr_status_t st = check_shape(A->M, A->K, A->b, A->dtype);
@@ -114,9 +151,13 @@ size_t bsr_prune_workspace_bytes(int64_t M, int64_t K, int32_t b) {
 
 size_t bsr_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec) {
     if (bsr_num_blocks(M, K, b) < 0 || N <= 0) return 0;
+    // the dense-rebuild tensor-core path is a candidate below the native block sizes
+    const bool dense = dense_tc_shape_ok(M, K, N) && (prec == BSR_PREC_FP32 ? b < 32 : b < 16);
+    const int kind = prec == BSR_PREC_FP32 ? 2 : prec == BSR_PREC_TF32 ? 0 : 1;
+    const size_t dws = dense ? dense_tc_layout(M, K, N, prec == BSR_PREC_BF16 ? 2 : 4, kind).total : 0;
     if (prec == BSR_PREC_FP32)
-        return std::max(bsrp::wgrad_simt_ws_bytes(M, K, b, N), bsrp::wgrad_x3_ws_bytes(M, K, b, N));
-    return bsrp::wgrad_tc_ws_bytes(M, K, b, N);
+        return std::max({bsrp::wgrad_simt_ws_bytes(M, K, b, N), bsrp::wgrad_x3_ws_bytes(M, K, b, N), dws});
+    return std::max(bsrp::wgrad_tc_ws_bytes(M, K, b, N), dws);
 }
 
 static bsr_status_t prune_impl(const void *X, int64_t M, int64_t K, int32_t b, int64_t k, int32_t dtype,
@@ -395,35 +436,10 @@ bsr_status_t bsr_wgrad_rows(const int32_t *rowptr, const int32_t *colidx, const 
                        "bsr_wgrad_rows launch");
 }
 
-/* 1 x b variant on the tensor cores: rebuild the masked rows densely, view them as a
- * keep-all 32 x 32 BSR and run the per-run tcgen05 kernel (FP32 grade for f32,
- * bf16 for bf16).  Workspace layout: [masked X: M*K elems][32x32 values: M*K elems]
- * [rowptr: M/32+1][colidx: (M/32)(K/32)][tensor-core split-K partials]. */
-namespace {
-constexpr int kRowsTcB = 32;
-size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-struct RowsTcWs {
-    size_t xm, vals, rp, ci, tc, total;
-};
-RowsTcWs rows_tc_layout(int64_t M, int64_t K, int64_t N, int es) {
-    RowsTcWs w{};
-    const int64_t nb = (M / kRowsTcB) * (K / kRowsTcB);
-    size_t o = 0;
-    w.xm = o;   o += align256((size_t)M * K * es);
-    w.vals = o; o += align256((size_t)M * K * es);
-    w.rp = o;   o += align256((size_t)(M / kRowsTcB + 1) * 4);
-    w.ci = o;   o += align256((size_t)nb * 4);
-    w.tc = o;
-    o += align256(es == 4 ? bsrp::wgrad_x3_ws_bytes(M, K, kRowsTcB, N) : bsrp::wgrad_tc_ws_bytes(M, K, kRowsTcB, N));
-    w.total = o;
-    return w;
-}
-}  // namespace
-
 size_t bsr_wgrad_rows_tc_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t x_dtype) {
     if (M <= 0 || K <= 0 || N <= 0 || !supported_b(b) || K % b || elem_size(x_dtype) == 0) return 0;
-    if (M % kRowsTcB || K % kRowsTcB || N % 128) return 0;
-    return rows_tc_layout(M, K, N, elem_size(x_dtype)).total;
+    if (!dense_tc_shape_ok(M, K, N)) return 0;
+    return dense_tc_layout(M, K, N, elem_size(x_dtype), x_dtype == BSR_DT_F32 ? 2 : 1).total;
 }
 
 bsr_status_t bsr_wgrad_rows_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnz, int64_t M,
@@ -432,30 +448,23 @@ bsr_status_t bsr_wgrad_rows_tc(const int32_t *rowptr, const int32_t *colidx, con
     bsr_status_t st = check_rows(M, K, b, x_dtype);
     if (st != BSR_OK) return st;
     if (dy_dtype != x_dtype) return fail(BSR_ERR_UNSUPPORTED, "tensor-core 1 x b dW needs dY in the dtype of X");
-    if (M % kRowsTcB || K % kRowsTcB)
-        return fail(BSR_ERR_UNSUPPORTED, "tensor-core 1 x b dW needs 32 | M and 32 | K (M=%lld, K=%lld)", (long long)M,
-                    (long long)K);
-    if (N <= 0 || N % 128) return fail(BSR_ERR_UNSUPPORTED, "tensor-core 1 x b dW needs N %% 128 == 0 (N=%lld)", (long long)N);
+    if (!dense_tc_shape_ok(M, K, N))
+        return fail(BSR_ERR_UNSUPPORTED, "tensor-core 1 x b dW needs 32 | M, 32 | K, N %% 128 == 0 (M=%lld, K=%lld, N=%lld)",
+                    (long long)M, (long long)K, (long long)N);
     if (!rowptr || !dY || !dW) return fail(BSR_ERR_INVALID_ARG, "rowptr, dY or dW is NULL");
     if (nnz > 0 && (!colidx || !values)) return fail(BSR_ERR_INVALID_ARG, "colidx / values are NULL with nnz > 0");
     if (accumulate != 0 && accumulate != 1) return fail(BSR_ERR_INVALID_ARG, "accumulate must be 0 or 1");
     if (!aligned16(dY) || !aligned16(dW)) return fail(BSR_ERR_ALIGNMENT, "dY or dW is not 16-byte aligned");
     const int es = elem_size(x_dtype);
-    const RowsTcWs w = rows_tc_layout(M, K, N, es);
+    const DenseTcWs w = dense_tc_layout(M, K, N, es, es == 4 ? 2 : 1);
     if (!ws || ws_bytes < w.total)
         return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, w.total);
     if (!aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
-    char *base = static_cast<char *>(ws);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    void *xm = base + w.xm;
-    cudaError_t e = bsrp::launch_decompress_rows(rowptr, colidx, nnz > 0 ? values : nullptr, M, K, b, es, xm, s);
+    cudaError_t e = bsrp::launch_decompress_rows(rowptr, colidx, nnz > 0 ? values : nullptr, M, K, b, es,
+                                                 static_cast<char *>(ws) + w.xm, s);
     if (e != cudaSuccess) return cuda_status(e, "bsr_wgrad_rows_tc (masked rows)");
-    const int64_t nbk = (M / kRowsTcB) * (K / kRowsTcB);
-    int32_t *rp = reinterpret_cast<int32_t *>(base + w.rp), *ci = reinterpret_cast<int32_t *>(base + w.ci);
-    e = bsrp::launch_prune(xm, M, K, kRowsTcB, es, nbk, rp, ci, base + w.vals, nullptr, s);  // k = N: one copy pass
-    if (e != cudaSuccess) return cuda_status(e, "bsr_wgrad_rows_tc (dense blocks)");
-    return cuda_status(bsrp::launch_wgrad_tc(rp, ci, base + w.vals, nbk, es == 4 ? 2 : 1, BSR_ALGO_TC_RUNS, M, K, kRowsTcB,
-                                             dY, N, dW, accumulate, base + w.tc, s),
+    return cuda_status(dense_tc_finish(M, K, es, es == 4 ? 2 : 1, dY, N, dW, accumulate, ws, w, s),
                        "bsr_wgrad_rows_tc launch");
 }
 
@@ -509,7 +518,7 @@ bsr_status_t bsr_wgrad_algo(const bsr_t *A, const void *dY, int32_t dy_dtype, in
     if (N <= 0 || N > (int64_t(1) << 30)) return fail(BSR_ERR_SHAPE, "N=%lld out of range", (long long)N);
     if (!dY || !dW) return fail(BSR_ERR_INVALID_ARG, "dY or dW is NULL");
     if (accumulate != 0 && accumulate != 1) return fail(BSR_ERR_INVALID_ARG, "accumulate must be 0 or 1");
-    if (algo < BSR_ALGO_AUTO || algo > BSR_ALGO_SIMT) return fail(BSR_ERR_INVALID_ARG, "algo %d is not a bsr_algo_t", algo);
+    if (algo < BSR_ALGO_AUTO || algo > BSR_ALGO_TC_DENSE) return fail(BSR_ERR_INVALID_ARG, "algo %d is not a bsr_algo_t", algo);
     if (!aligned16(dY) || !aligned16(dW)) return fail(BSR_ERR_ALIGNMENT, "dY or dW is not 16-byte aligned");
     if ((N * esy) % 16 != 0 || (N * 4) % 16 != 0)
         return fail(BSR_ERR_ALIGNMENT, "row pitch of dY/dW (N=%lld) is not a multiple of 16 bytes", (long long)N);
@@ -519,6 +528,26 @@ bsr_status_t bsr_wgrad_algo(const bsr_t *A, const void *dY, int32_t dy_dtype, in
     if (A->K / A->b > 65535)
         return fail(BSR_ERR_UNSUPPORTED, "K/b must stay below 65536 (K/b=%lld)", (long long)(A->K / A->b));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (prec != BSR_PREC_FP32 && prec != BSR_PREC_TF32 && prec != BSR_PREC_BF16)
+        return fail(BSR_ERR_INVALID_ARG, "prec %d is not a bsr_prec_t", prec);
+    // dense rebuild on the tensor cores: chosen by AUTO below the native block sizes
+    const int dkind = prec == BSR_PREC_FP32 ? 2 : prec == BSR_PREC_TF32 ? 0 : 1;
+    const int dwant = prec == BSR_PREC_BF16 ? BSR_DT_BF16 : BSR_DT_F32;
+    const bool dense_ok = A->dtype == dwant && dy_dtype == dwant && dense_tc_shape_ok(A->M, A->K, N);
+    const bool dense_auto = dense_ok && algo == BSR_ALGO_AUTO && (prec == BSR_PREC_FP32 ? A->b < 32 : A->b < 16);
+    if (algo == BSR_ALGO_TC_DENSE || dense_auto) {
+        if (!dense_ok)
+            return fail(BSR_ERR_UNSUPPORTED, "dense-rebuild tensor-core dW needs %s values and dY, 32 | M, 32 | K, "
+                                             "N %% 128 == 0", dwant == BSR_DT_BF16 ? "bf16" : "fp32");
+        const DenseTcWs w = dense_tc_layout(A->M, A->K, N, elem_size(dwant), dkind);
+        st = check_wgrad_ws(w.total, ws, ws_bytes, dW, dw_bytes);
+        if (st != BSR_OK) return st;
+        cudaError_t e = bsrp::launch_decompress(A->rowptr, A->colidx, A->nnzb ? A->values : nullptr, A->M, A->K, A->b,
+                                                esx, static_cast<char *>(ws) + w.xm, s);
+        if (e != cudaSuccess) return cuda_status(e, "bsr_wgrad (dense rebuild)");
+        return cuda_status(dense_tc_finish(A->M, A->K, esx, dkind, dY, N, dW, accumulate, ws, w, s),
+                           "bsr_wgrad (dense rebuild, tensor cores) launch");
+    }
     if (prec == BSR_PREC_FP32) {
         // FP32 grade: 3xTF32 tensor cores where implemented, else FFMA
         const bool x3 = A->dtype == BSR_DT_F32 && dy_dtype == BSR_DT_F32 &&
@@ -539,7 +568,6 @@ bsr_status_t bsr_wgrad_algo(const bsr_t *A, const void *dY, int32_t dy_dtype, in
                                                    A->b, dY, esy, N, dW, accumulate, ws, s),
                            "bsr_wgrad (fp32) launch");
     }
-    if (prec != BSR_PREC_TF32 && prec != BSR_PREC_BF16) return fail(BSR_ERR_INVALID_ARG, "prec %d is not a bsr_prec_t", prec);
     const int want = prec == BSR_PREC_TF32 ? BSR_DT_F32 : BSR_DT_BF16;
     if (A->dtype != want || dy_dtype != want)
         return fail(BSR_ERR_UNSUPPORTED, "%s tensor-core path needs %s values and dY", prec == BSR_PREC_TF32 ? "TF32" : "BF16",

@@ -71,9 +71,13 @@ def test_storage_bytes_matches_oracle(lib, M, b, k):
 def test_workspace_query(lib):
     assert lib.bsr_prune_workspace_bytes(256, 256, 16) >= 2 * 256 * 4
     assert lib.bsr_prune_workspace_bytes(100, 256, 16) == 0
-    # FP32 path: one 128 x 128 tile set, 16 block rows -> 2 splits of partial dW
-    assert lib.bsr_wgrad_workspace_bytes(256, 256, 16, 256, 0) == 2 * 256 * 256 * 4
-    assert lib.bsr_wgrad_workspace_bytes(16, 256, 16, 256, 0) == 0  # one block row: no split
+    # FP32 grade at b = 16: the FFMA kernel's split partials (2 x K x N) or the dense
+    # rebuild's masked X + 32 x 32 values + indices + tensor-core partials, whichever is larger
+    need = lib.bsr_wgrad_workspace_bytes(256, 256, 16, 256, 0)
+    assert need >= 2 * 256 * 256 * 4 and need >= 2 * 256 * 256 * 4 + 4 * (256 // 32 + 1)
+    # N = 200 (not a multiple of 128): FFMA only; one block row: no split
+    assert lib.bsr_wgrad_workspace_bytes(16, 256, 16, 200, 0) == 0
+    assert lib.bsr_wgrad_workspace_bytes(256, 256, 16, 200, 0) == 2 * 256 * 200 * 4
 
 
 # ------------------------------------------------------------ validation errors

@@ -49,3 +49,30 @@ def test_native_arm_c4_one_gpu():
     assert d["config"]["rows_per_rank"] == 1024 * 196
     assert d["gpu_launches_per_step"] >= 48 * 3
     assert d["value"] > 0 and d["ms_per_step"] > 0
+
+
+@pytest.mark.gpu
+def test_native_arm_two_ranks_control_flow():
+    """--gpus 2 re-launches itself under torch.distributed.run; with the gloo test hook
+    both ranks share the one GPU, which exercises the N > 1 control flow (barriers,
+    max / sum over ranks, the dW all-reduce, the JSON line from rank 0 only)."""
+    env = dict(os.environ, BSRP_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "6", "--warmup", "3",
+                          "--no-cpu-baseline", "--e2e-steps", "2"], capture_output=True, text=True, timeout=900,
+                         cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2" and "allreduce" in d["kernels"]
+
+
+@pytest.mark.gpu
+def test_native_arm_c4_two_ranks_control_flow():
+    env = dict(os.environ, BSRP_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C4", "--gpus", "2", "--steps",
+                          "3", "--warmup", "3", "--keep", "0.2"], capture_output=True, text=True, timeout=1200,
+                         cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["rows_per_rank"] == 1024 * 196 // 2

@@ -32,21 +32,26 @@ TOL = {"fp32": 1e-5, "tf32": 5e-3, "bf16": 1e-4}
 UNSUPPORTED = 3  # BSR_ERR_UNSUPPORTED
 
 
-@pytest.fixture(params=["runs", "span", "auto"])
+@pytest.fixture(params=["runs", "span", "dense", "auto"])
 def algo(request):
-    """Every case runs on both tcgen05 dW kernels -- the per-run kernel and the span
-    kernel (CTA-pair MMAs) -- and on the library's own per-shape choice."""
+    """Every case runs on every tcgen05 dW family -- the per-run kernel, the span
+    kernel (CTA-pair MMAs), the dense rebuild (keep-all 32 x 32 view of the masked X)
+    -- and on the library's own per-shape choice."""
     return request.param
 
 
-def tc_supported(prec, b, algo):
+def tc_supported(prec, b, algo, M, K, N):
     """tf32 / bf16: b in {16, 32, 64} (tf32 b = 16 only pairs blocks in the span
-    kernel); FP32 grade on the tensor cores: the per-run kernel at b in {32, 64}
-    (auto falls back to FFMA elsewhere, still graded at 1e-5)."""
+    kernel); FP32 grade on the tensor cores: the per-run kernel at b in {32, 64};
+    dense rebuild: any b with 32 | M, 32 | K, N % 128 == 0.  auto always works
+    (FFMA for the FP32 grade when nothing else applies)."""
+    dense_ok = M % 32 == 0 and K % 32 == 0 and N % 128 == 0
+    if algo == "dense":
+        return dense_ok
     if prec == "fp32":
         return algo == "auto" or (algo == "runs" and b in (32, 64))
     if b < 16:
-        return False
+        return algo == "auto" and dense_ok
     if prec == "tf32" and b == 16 and algo == "runs":
         return False
     return True
@@ -61,7 +66,7 @@ def run_tc(M, K, N, b, k, prec, algo, family="gelu", seed=0, accumulate=False, m
     bf = prec == "bf16"
     A = bp.prune(to_torch(X, bf16=bf), b, k=k)
     dYt = to_torch(dY, bf16=bf)
-    if not tc_supported(prec, b, algo):
+    if not tc_supported(prec, b, algo, M, K, N):
         with pytest.raises(bp.BsrError) as ei:
             bp.wgrad(A, dYt, prec=prec, algo=algo)
         assert ei.value.status == UNSUPPORTED
@@ -96,7 +101,7 @@ PRECS = ["fp32", "tf32", "bf16"]
 
 
 @pytest.mark.parametrize("prec", PRECS)
-@pytest.mark.parametrize("b", [16, 32, 64])
+@pytest.mark.parametrize("b", [4, 8, 16, 32, 64])
 @pytest.mark.parametrize("keep", [0.1, 0.5, 1.0])
 @pytest.mark.parametrize("shape", [(37, 6, 128), (5, 3, 256), (64, 20, 384)])  # (block rows, block cols, N)
 def test_wgrad_tc_random(algo, prec, b, keep, shape):

@@ -228,6 +228,7 @@ def sweep_rows(out, hbm, reps=6, nsets=3):
                 t_p = timed(lambda j: bp.prune_rows(Xs[j], b, keep, sample_rows=S), Xs, reps)
                 dW = torch.empty(K, N, device="cuda")
                 t_w = timed(lambda j: bp.wgrad_rows(As[j], dYs[j], out=dW), Xs, reps)
+                t_wf = timed(lambda j: bp.wgrad_rows(As[j], dYs[j], out=dW, tensor_cores=False), Xs, reps)
                 D = torch.empty(M, K, device="cuda")
                 t_d = timed(lambda j: bp.decompress_rows(As[j], out=D), Xs, reps)
                 ref = bp.decompress_rows(As[0]).double().T @ dYs[0].double()
@@ -237,6 +238,9 @@ def sweep_rows(out, hbm, reps=6, nsets=3):
                 row = dict(config="f2-rows", layer=lname, M=M, K=K, N=N, b=b, keep=keep, k=k, sample_rows=S,
                            prune_ms=t_p, prune_gbs=pb / (t_p * 1e-3) / 1e9, prune_hbm_frac=pb / (t_p * 1e-3) / 1e9 / hbm,
                            wgrad_ms=t_w, wgrad_tflops=2 * k * b * N / (t_w * 1e-3) / 1e12,
+                           wgrad_path="tensor cores (dense rebuild, FP32 grade)" if
+                           bp._lib.load().bsr_wgrad_rows_tc_workspace_bytes(M, K, b, N, 0) else "FFMA",
+                           wgrad_ffma_ms=t_wf,
                            decompress_ms=t_d, decompress_gbs=(bsr + 4 * M * K) / (t_d * 1e-3) / 1e9,
                            act_bytes_saved=4 * M * K - bsr, check_rel_err=err)
                 rows.append(row)
