@@ -156,6 +156,10 @@ BSR_API size_t bsr_prune_workspace_bytes(int64_t M, int64_t K, int32_t b);
  * the result is deterministic.  Must be 16-byte aligned and must not overlap dW. */
 BSR_API size_t bsr_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec);
 
+/* The same query for an explicit kernel family of bsr_wgrad_algo (bsr_algo_t);
+ * bsr_wgrad_workspace_bytes = this with BSR_ALGO_AUTO. */
+BSR_API size_t bsr_wgrad_algo_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec, int32_t algo);
+
 /* ---- device work ------------------------------------------------------------ */
 
 /* Prune X (M x K, row-major, `dtype`) to its top-k blocks by l2 norm and pack

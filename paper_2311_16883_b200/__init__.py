@@ -240,7 +240,7 @@ def wgrad(A: BSR, dY: torch.Tensor, prec: str = "fp32", out: torch.Tensor | None
     else:
         _check_dense_out(out, (A.K, N), torch.float32, dY.device, "out")
     p = PREC[prec]
-    ws_bytes = lib.bsr_wgrad_workspace_bytes(A.M, A.K, A.b, N, p)
+    ws_bytes = lib.bsr_wgrad_algo_workspace_bytes(A.M, A.K, A.b, N, p, ALGO[algo])
     ws = workspace(ws_bytes, dY.device, stream=stream) if ws_bytes else None
     cs = A.c_struct()
     _lib.check(lib.bsr_wgrad_algo(ctypes.byref(cs), dY.data_ptr(), _dt(dY), N, out.data_ptr(), int(accumulate), p,

@@ -149,15 +149,20 @@ size_t bsr_prune_workspace_bytes(int64_t M, int64_t K, int32_t b) {
     return bsrp::prune_ws_layout(N).total;
 }
 
-size_t bsr_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec) {
+size_t bsr_wgrad_algo_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec, int32_t algo) {
     if (bsr_num_blocks(M, K, b) < 0 || N <= 0) return 0;
-    // the dense-rebuild tensor-core path is a candidate below the native block sizes
-    const bool dense = dense_tc_shape_ok(M, K, N) && (prec == BSR_PREC_FP32 ? b < 32 : b < 16);
+    // the dense-rebuild tensor-core path: requested, or AUTO's choice below the native block sizes
+    const bool dense = dense_tc_shape_ok(M, K, N) &&
+                       (algo == BSR_ALGO_TC_DENSE || (algo == BSR_ALGO_AUTO && (prec == BSR_PREC_FP32 ? b < 32 : b < 16)));
     const int kind = prec == BSR_PREC_FP32 ? 2 : prec == BSR_PREC_TF32 ? 0 : 1;
     const size_t dws = dense ? dense_tc_layout(M, K, N, prec == BSR_PREC_BF16 ? 2 : 4, kind).total : 0;
     if (prec == BSR_PREC_FP32)
         return std::max({bsrp::wgrad_simt_ws_bytes(M, K, b, N), bsrp::wgrad_x3_ws_bytes(M, K, b, N), dws});
     return std::max(bsrp::wgrad_tc_ws_bytes(M, K, b, N), dws);
+}
+
+size_t bsr_wgrad_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec) {
+    return bsr_wgrad_algo_workspace_bytes(M, K, b, N, prec, BSR_ALGO_AUTO);
 }
 
 static bsr_status_t prune_impl(const void *X, int64_t M, int64_t K, int32_t b, int64_t k, int32_t dtype,

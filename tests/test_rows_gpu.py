@@ -144,7 +144,7 @@ def test_wgrad_rows_tensor_cores(bf16, keep):
     """The 1 x b variant's dW on the tensor cores (kept rows rebuilt densely, keep-all
     32 x 32 BSR, per-run tcgen05 kernel: FP32 grade for f32, bf16 for bf16) against
     the oracle on the GPU's own selection, and against the FFMA kernel."""
-    S, nsamp, K, N, b = 196, 4, 384, 256, 16
+    S, nsamp, K, N, b = 196, 8, 384, 256, 16  # M = 1568 = 49 x 32
     M = S * nsamp
     X = synth.f_aff(M, K, 55)
     dY = synth.grad_out(M, N, 55)
