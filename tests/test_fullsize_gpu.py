@@ -273,3 +273,69 @@ def test_two_ranks_dw_allreduce(prec):
         assert p.exitcode == 0
     assert np.array_equal(res[0][1].view(np.int32), res[1][1].view(np.int32))  # every rank holds the same sum
     assert oracle.rel_frobenius(res[0][1], ref) <= TOL[prec]
+
+
+@pytest.mark.parametrize("b", [4, 16])
+def test_dense_rebuild_fp32_grade_full_size(b):
+    """The dense-rebuild tensor-core path (AUTO for the FP32 grade below b = 32) at the
+    full S12 fc1 size, element-wise against the oracle (masked-X BLAS form)."""
+    c = synth.CONFIGS["C2"]
+    M, K, N = c["M"], c["K"], c["N"]
+    X = synth.activation(c["family"], M, K, synth.seed_for(2, 1))
+    dY = synth.grad_out(M, N, synth.seed_for(2, 1))
+    k = oracle.keep_count(oracle.num_blocks(M, K, b), 0.5)
+    k = gap_k(X, b, k)
+    ref = oracle.prune(X, b, k)
+    want = oracle.wgrad_masked(ref["rowptr"], ref["colidx"], ref["values"], M, K, b, dY)
+    A = bp.prune(to_torch(X), b, k=k)
+    out = torch.full((K, N), float("nan"), device="cuda")
+    bp.wgrad(A, to_torch(dY), prec="fp32", algo="dense", out=out)
+    auto = bp.wgrad(A, to_torch(dY), prec="fp32")  # AUTO picks the same path here
+    got = out.cpu().numpy()
+    assert oracle.rel_frobenius(got, want) <= 1e-5
+    assert torch.equal(auto.view(torch.int32), out.view(torch.int32))
+
+
+@pytest.mark.parametrize("prec,algo", [("fp32", "runs"), ("fp32", "simt"), ("fp32", "dense"), ("tf32", "runs"),
+                                       ("tf32", "span"), ("bf16", "runs"), ("bf16", "span"), ("bf16", "dense")])
+def test_dw_deterministic(prec, algo):
+    """Every dW family is deterministic: split partials are summed in split order, so
+    repeated launches (and a launch on another stream) give the same bits."""
+    c = synth.CONFIGS["C2"]
+    M, K, N, b = c["M"], c["K"], c["N"], c["b"]
+    bf = prec == "bf16"
+    X = synth.activation(c["family"], M, K, 7)
+    dY = synth.grad_out(M, N, 7)
+    if bf:
+        X, dY = synth.to_bf16_bits(X), synth.to_bf16_bits(dY)
+    A = bp.prune(to_torch(X, bf16=bf), b, keep=0.5)
+    dYt = to_torch(dY, bf16=bf)
+    first = bp.wgrad(A, dYt, prec=prec, algo=algo)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        other = bp.wgrad(A, dYt, prec=prec, algo=algo, stream=s)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        again = bp.wgrad(A, dYt, prec=prec, algo=algo)
+        assert torch.equal(again.view(torch.int32), first.view(torch.int32))
+    assert torch.equal(other.view(torch.int32), first.view(torch.int32))
+
+
+def test_rows_tensor_cores_full_s12_batch():
+    """The 1 x b variant's tensor-core dW at the full S12 fc1 batch (128 samples),
+    against the oracle's own per-sample selection (integer-valued X: exact fp32 sums,
+    ties by the flat-index rule, so the GPU must select exactly the oracle's set)."""
+    S, K, N, b = 196, 384, 1536, 16
+    M = S * 128
+    X = synth.ints(M, K, 57)
+    dY = synth.grad_out(M, N, 57)
+    ks = oracle.keep_count(S * K // b, 0.5)
+    ref = oracle.prune_per_sample(X, b, ks, S)
+    A = bp.prune_rows(to_torch(X), b, 0.5, sample_rows=S)
+    got = bp.wgrad_rows(A, to_torch(dY), tensor_cores=True).cpu().numpy()
+    np.testing.assert_array_equal(A.rowptr.cpu().numpy(), ref["rowptr"])
+    np.testing.assert_array_equal(A.colidx.cpu().numpy(), ref["colidx"])
+    Xm = oracle.decompress(ref["rowptr"], ref["colidx"], ref["values"].reshape(-1, 1, b), M, K, 1, b)
+    want = Xm.astype(np.float64).T @ dY.astype(np.float64)  # (X * mask)^T dY in fp64 (pinned form)
+    assert oracle.rel_frobenius(got, want) <= 1e-5
