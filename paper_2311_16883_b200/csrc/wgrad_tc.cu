@@ -315,8 +315,12 @@ struct Cfg {
     // one TMEM A buffer, one trip through every barrier.  The per-step
     // synchronisation (each mbarrier wait costs ~100 cycles even when the phase
     // has completed) is paid once per 64 rows instead of once per block row.
-    // FP32 grade: one block row per step (its A buffer holds hi and lo).
-    static constexpr int R = (X3 || B >= 64) ? 1 : 64 / B;
+    // FP32 grade: one block row per step (its A buffer holds hi and lo).  tf32 at
+    // b = 32: one block row too -- a 32-column A buffer leaves room for four of them
+    // next to a 384-column accumulator (two with 64-row steps); measured C2 76.7 ->
+    // 65.8 us, B24 fc1 shard 245 -> 207 us.  bf16 keeps 64-row steps (R = 1 measured
+    // slower there: 48 -> 57 us; its 64-row A buffer is 32 columns already).
+    static constexpr int R = (X3 || B >= 64 || (KIND == 0 && B == 32)) ? 1 : 64 / B;
     static constexpr int SROWS = R * B;                     // dY rows per step
     static constexpr int A_STEP = R * A_ROW;                // TMEM columns of one step's A buffer
     static constexpr int SLAB = SROWS * 128 * ES;           // one dY slab (SROWS rows x 128 columns, row-major)

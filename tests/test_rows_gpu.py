@@ -33,7 +33,7 @@ def oracle_rows_ref(X, b, keep, S, A, bf16=False):
     K = X.shape[1]
     Xf = synth.bf16_bits_to_f32(X) if bf16 else X
     ks = oracle.keep_count(S * K // b, keep)
-    if not _gap_ok(Xf, b, ks, S, rel=2e-4):
+    if not _gap_ok(Xf, b, ks, S, rel=1e-5):  # fp32 sums of <= 64 squares: error < 4e-6 relative
         pytest.skip("fp32 segment sums too close at the boundary for this seed")
     ref = oracle.prune_per_sample(X, b, ks, S)
     np.testing.assert_array_equal(A.rowptr.cpu().numpy(), ref["rowptr"])
