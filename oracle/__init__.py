@@ -91,6 +91,10 @@ def _load():
         lib.orc_wgrad_entries.restype = i32
         lib.orc_wgrad_entries.argtypes = [vp, vp, vp, i32, i64, i64, i64, i64, vp, i32, i64,
                                           vp, vp, i64, vp]
+        lib.orc_swap_uniform.restype = dbl
+        lib.orc_swap_uniform.argtypes = [ctypes.c_uint64, i64]
+        lib.orc_select_topk_stochastic.restype = i32
+        lib.orc_select_topk_stochastic.argtypes = [vp, i64, i64, i64, dbl, ctypes.c_uint64, vp]
         lib.orc_affine_wgrad.restype = i32
         lib.orc_affine_wgrad.argtypes = [vp, vp, vp, i32, i64, i64, i64, i64, vp, i32, vp]
         _lib = lib
@@ -260,6 +264,26 @@ def affine_wgrad(rowptr, colidx, values, M: int, K: int, b: int, dY: np.ndarray)
                                     _dtype_code(values), M, K, b, b, _ptr(dY), _dtype_code(dY), _ptr(out)),
            "affine_wgrad")
     return out
+
+
+def swap_uniform(seed: int, i: int) -> float:
+    """The counter-based uniform u_i of the stochastic boundary swap (reading R19)."""
+    return float(_load().orc_swap_uniform(seed, i))
+
+
+def prune_stochastic(X: np.ndarray, b: int, k: int, window: int, p: float, seed: int):
+    """Top-k with stochastic boundary swapping (reading R19): pair i of
+    the w' = min(window, k, N-k) pairs (rank k-1-i, rank k+i) swaps kept/pruned iff
+    swap_uniform(seed, i) < p.  Returns dict(rowptr, colidx, values, mask)."""
+    X = np.ascontiguousarray(X)
+    M, K = X.shape
+    sumsq = block_sumsq(X, b)
+    N = sumsq.size
+    mask = np.empty(N, dtype=np.uint8)
+    _check(_load().orc_select_topk_stochastic(_ptr(np.ascontiguousarray(sumsq)), N, k, window, float(p), seed,
+                                             _ptr(mask)), "select_topk_stochastic")
+    rowptr, colidx, values = build_bsr(X, mask, b)
+    return {"rowptr": rowptr, "colidx": colidx, "values": values, "mask": mask}
 
 
 def wgrad_rect(rowptr, colidx, values, M: int, K: int, br: int, bc: int, dY: np.ndarray) -> np.ndarray:

@@ -297,3 +297,52 @@ int orc_affine_wgrad(const int32_t *rowptr, const int32_t *colidx, const void *v
         }
     return 0;
 }
+
+/* ---- stochastic boundary swapping ---------------------------
+ * "One could imagine randomly swapping blocks near the top-k threshold, resulting
+ * in some blocks above the threshold being pruned anyway, and vice-versa below
+ * threshold" (future work in the paper).  Reading R19:
+ * rank the blocks by (norm desc, flat index asc) (O4); the deterministic top-k
+ * keeps ranks [0, k).  With w' = min(window, k, N - k), pair i < w' couples rank
+ * k-1-i (kept) with rank k+i (pruned); the pair swaps -- the first pruned, the
+ * second kept -- iff u_i < p, where u_i is the counter-based uniform
+ *   z = seed + (i + 1) * 0x9E3779B97F4A7C15 (mod 2^64), splitmix64 finaliser,
+ *   u_i = (z >> 11) * 2^-53.
+ * Exactly k blocks stay kept.  mask[f] = 1 for kept blocks. */
+static uint64_t orc_splitmix(uint64_t seed, uint64_t i)
+{
+    uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+double orc_swap_uniform(uint64_t seed, int64_t i)
+{
+    return (double)(orc_splitmix(seed, (uint64_t)i) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+int orc_select_topk_stochastic(const double *sumsq, int64_t N, int64_t k, int64_t window, double p,
+                               uint64_t seed, uint8_t *mask)
+{
+    if (N < 0 || k < 0 || k > N || window < 0 || !(p >= 0.0 && p <= 1.0)) return -2;
+    double *norm = (double *)malloc((size_t)(N > 0 ? N : 1) * sizeof(double));
+    int64_t *order = (int64_t *)malloc((size_t)(N > 0 ? N : 1) * sizeof(int64_t));
+    if (!norm || !order) { free(norm); free(order); return -2; }
+    for (int64_t i = 0; i < N; ++i) { norm[i] = sqrt(sumsq[i]); order[i] = i; }
+    g_norm = norm;  /* the same ranking as orc_select_topk (O4) */
+    qsort(order, (size_t)N, sizeof(int64_t), orc_cmp);
+    for (int64_t i = 0; i < N; ++i) mask[i] = 0;
+    for (int64_t r = 0; r < k; ++r) mask[order[r]] = 1;
+    int64_t w = window;
+    if (w > k) w = k;
+    if (w > N - k) w = N - k;
+    for (int64_t i = 0; i < w; ++i)
+        if (orc_swap_uniform(seed, i) < p) {
+            mask[order[k - 1 - i]] = 0;
+            mask[order[k + i]] = 1;
+        }
+    free(norm);
+    free(order);
+    return 0;
+}

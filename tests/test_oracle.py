@@ -427,3 +427,85 @@ def test_wgrad_rect_equals_masked_matmul():
     dW = oracle.wgrad_rect(ref["rowptr"], ref["colidx"], ref["values"], S * nsamp, K, 1, b, dY)
     Xm = X.astype(np.float64) * np.repeat(ref["mask"].reshape(S * nsamp, K // b), b, axis=1)
     np.testing.assert_allclose(dW, Xm.T @ dY.astype(np.float64), rtol=1e-12, atol=1e-12)
+
+
+# ------------------------------------------------------------------ P13 stochastic boundary swapping (R19)
+def _rank_order(s):
+    """Flat indices by (value desc, index asc): numpy lexsort, not the oracle's qsort."""
+    s = np.asarray(s, np.float64)
+    return np.lexsort((np.arange(s.size), -s))
+
+
+def test_swap_uniform_is_splitmix64():
+    """u_i = (splitmix64 output >> 11) * 2^-53 with the generator's state starting
+    at `seed`: the published first outputs of splitmix64 from state 0 are
+    0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F."""
+    for i, v in enumerate((0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F)):
+        assert oracle.swap_uniform(0, i) == (v >> 11) / 2.0 ** 53
+    u = np.array([oracle.swap_uniform(12345, i) for i in range(20000)])
+    assert u.min() >= 0.0 and u.max() < 1.0
+    assert abs(u.mean() - 0.5) < 0.01 and abs(u.var() - 1 / 12) < 0.005
+
+
+def test_stochastic_p0_is_topk():
+    """p = 0: no pair swaps, the selection is the deterministic top-k."""
+    rng = np.random.default_rng(5)
+    X = synth.ints(16 * 8, 12 * 8, seed=5, lo=-9, hi=9)
+    for k, w in ((10, 3), (96, 50), (0, 4), (192, 4), (50, 0)):
+        r = oracle.prune_stochastic(X, 8, k, w, 0.0, int(rng.integers(1 << 62)))
+        np.testing.assert_array_equal(r["mask"], oracle.prune(X, 8, k)["mask"])
+
+
+@pytest.mark.parametrize("k,w", [(10, 3), (100, 50), (5, 9), (190, 9), (96, 96)])
+def test_stochastic_p1_swaps_whole_window(k, w):
+    """p = 1: every pair swaps -- kept = ranks [0, k-w') and [k, k+w'), w' = min(w, k, N-k)."""
+    X = synth.ints(16 * 4, 12 * 4, seed=k + w, lo=-3, hi=3)  # ties: the rank order decides
+    N = 16 * 12
+    s = oracle.block_sumsq(X, 4)
+    order = _rank_order(s)
+    wp = min(w, k, N - k)
+    want = np.zeros(N, np.uint8)
+    want[order[: k - wp]] = 1
+    want[order[k: k + wp]] = 1
+    r = oracle.prune_stochastic(X, 4, k, w, 1.0, 77)
+    np.testing.assert_array_equal(r["mask"], want)
+
+
+def test_stochastic_pairs_and_counts():
+    """Any p: exactly k kept; ranks < k - w' always kept, ranks >= k + w' never;
+    a kept rank k+i comes with a pruned rank k-1-i (pairs), and the swapped pairs
+    are the i with u_i < p."""
+    X = synth.ints(40 * 8, 30 * 8, seed=9, lo=-20, hi=20)
+    s = oracle.block_sumsq(X, 8)
+    N = s.size
+    order = _rank_order(s)
+    rank = np.empty(N, np.int64)
+    rank[order] = np.arange(N)
+    for k, w, p, seed in ((600, 200, 0.3, 1), (300, 1000, 0.7, 2), (1100, 100, 0.5, 3)):
+        m = oracle.prune_stochastic(X, 8, k, w, p, seed)["mask"].astype(bool)
+        wp = min(w, k, N - k)
+        assert m.sum() == k
+        assert m[rank < k - wp].all() and not m[rank >= k + wp].any()
+        for i in range(wp):
+            sw = oracle.swap_uniform(seed, i) < p
+            assert m[order[k - 1 - i]] == (not sw) and m[order[k + i]] == sw
+
+
+def test_stochastic_swap_fraction():
+    """The swapped fraction of the w' pairs is p within 5 binomial sigmas."""
+    X = synth.f_aff(200 * 8, 40 * 8, seed=4)
+    k, w = 4000, 3000
+    for p in (0.1, 0.5, 0.9):
+        m = oracle.prune_stochastic(X, 8, k, w, p, 11)["mask"].astype(bool)
+        top = oracle.prune(X, 8, k)["mask"].astype(bool)
+        swapped = int((top & ~m).sum())
+        assert abs(swapped - p * w) < 5 * np.sqrt(w * p * (1 - p)), (p, swapped)
+
+
+def test_stochastic_bsr_is_masked_x():
+    """The BSR of the stochastic selection decompresses to X masked by it (O5/O6)."""
+    X = synth.ints(12 * 4, 9 * 4, seed=2, lo=-5, hi=5)
+    r = oracle.prune_stochastic(X, 4, 50, 20, 0.5, 3)
+    D = oracle.decompress(r["rowptr"], r["colidx"], r["values"], X.shape[0], X.shape[1], 4)
+    m = np.kron(r["mask"].reshape(12, 9), np.ones((4, 4))).astype(bool)
+    np.testing.assert_array_equal(D, np.where(m, X, 0))
