@@ -72,8 +72,9 @@ def parse():
     ap.add_argument("--b", type=int, default=None)
     ap.add_argument("--keep", type=float, default=None)
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of CUDA-graph replays")
-    ap.add_argument("--order", choices=["pwd", "pdw"], default="pwd",
-                    help="kernel order inside a step: prune-wgrad-decompress or prune-decompress-wgrad")
+    ap.add_argument("--order", choices=["pwd", "pdw", "overlap"], default="pwd",
+                    help="kernel order inside a step: prune-wgrad-decompress, prune-decompress-wgrad, or the "
+                         "decompress on a second stream beside the wgrad (both only read the BSR)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
@@ -410,7 +411,8 @@ def run_native(a):
     dWs = [torch.empty(K, N, dtype=torch.float32, device=dev) for _ in range(nsets)]
     Xds = [torch.empty(M, K, dtype=tdt, device=dev) for _ in range(nsets)]
     s = torch.cuda.Stream(device=dev)  # every launch (eager warm-up, capture, replay) on this stream
-    phases = ["prune", "wgrad", "decompress"] if a.order == "pwd" else ["prune", "decompress", "wgrad"]
+    s2 = torch.cuda.Stream(device=dev)  # --order overlap: the decompress beside the wgrad
+    phases = ["prune", "decompress", "wgrad"] if a.order == "pdw" else ["prune", "wgrad", "decompress"]
 
     def phase_fn(j, p, prec=None):
         if p == "prune":
@@ -420,6 +422,14 @@ def run_native(a):
         return lambda: bp.decompress(bsrs[j], out=Xds[j], stream=s)
 
     def full_step(j):
+        if a.order == "overlap":  # fork after the prune, join before the step ends
+            phase_fn(j, "prune")()
+            s2.wait_stream(s)
+            with torch.cuda.stream(s2):
+                bp.decompress(bsrs[j], out=Xds[j], stream=s2)
+            phase_fn(j, "wgrad")()
+            s.wait_stream(s2)
+            return
         for p in phases:
             phase_fn(j, p)()
 
@@ -649,7 +659,8 @@ def run_native(a):
                             "bsr_bytes": metrics.bsr_bytes(M, b, k, s_x)},
         "work_per_step": {"alg_bytes": work.bytes, "wgrad_flops": work.wgrad_flops, "k": k, "nblocks": nblocks,
                           "r_ne": r_ne, "wgrad_flops_all_ranks_per_s": flops_all / (t_ms_max * 1e-3)},
-        "launch": "one CUDA graph per step (prune -> wgrad -> decompress)" if use_graph else "eager",
+        "launch": ("one CUDA graph per step (" + ("prune -> {wgrad || decompress on a second stream}"
+                   if a.order == "overlap" else " -> ".join(phases)) + ")") if use_graph else "eager",
         "kernel_timing": f"per kernel: one launch per rotating input set ({nsets}) back to back in one graph, "
                          "CUDA events around the replays (a second timed region after the step loop)",
         "gpu_launches": launches_per_step["step"] * a.steps,

@@ -181,6 +181,28 @@ BSR_API bsr_status_t bsr_prune(const void *X, int64_t M, int64_t K, int32_t b, d
 BSR_API bsr_status_t bsr_prune_k(const void *X, int64_t M, int64_t K, int32_t b, int64_t k,
                          int32_t dtype, bsr_t *out, void *ws, size_t ws_bytes, void *stream);
 
+/* Stochastic boundary swapping around the top-k threshold -- the paper's
+ * future-work variant: "randomly swapping blocks near the top-k threshold,
+ * resulting in some blocks above the threshold being pruned anyway, and
+ * vice-versa below threshold".  Reading R19 fixes it:
+ * rank the blocks by (sumsq desc, flat index asc) -- the bsr_prune order; let
+ * w = min(window, k, N - k).  Pair i < w couples rank k-1-i (kept by bsr_prune)
+ * with rank k+i (pruned by it) and swaps the two iff u_i < p, where
+ *   z = seed + (i + 1) * 0x9E3779B97F4A7C15 (mod 2^64), then the splitmix64
+ *   finaliser z ^= z >> 30, z *= 0xBF58476D1CE4E5B9, z ^= z >> 27,
+ *   z *= 0x94D049BB133111EB, z ^= z >> 31, and u_i = (z >> 11) * 2^-53.
+ * Exactly k blocks stay kept; p = 0 or w = 0 is bsr_prune_k.  The same seed
+ * gives the same selection on every call (the caller varies it per step).
+ * window: >= 0 with min(window, k, N - k) <= 4096 (else BSR_ERR_INVALID_ARG);
+ * p in [0, 1].  Outputs as bsr_prune_k.  ws: bsr_prune_stochastic_workspace_bytes
+ * bytes (a bsr_prune workspace of the same shape extended; zero-filled before
+ * first use and left zero-filled).  Stream-ordered, 9 kernels, no host sync,
+ * CUDA-graph capturable. */
+BSR_API size_t bsr_prune_stochastic_workspace_bytes(int64_t M, int64_t K, int32_t b);
+BSR_API bsr_status_t bsr_prune_stochastic(const void *X, int64_t M, int64_t K, int32_t b, int64_t k,
+                                  int64_t window, double p, uint64_t seed, int32_t dtype, bsr_t *out,
+                                  void *ws, size_t ws_bytes, void *stream);
+
 /* Test hook for step 1 alone: sumsq[N] (fp32, flat order) of every b x b block
  * of X, computed by the same kernel code as bsr_prune. */
 BSR_API bsr_status_t bsr_block_sumsq(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype,

@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from ._lib import ALGO, BsrError, DT_BF16, DT_F32, PREC
 
-__all__ = ["BSR", "BsrError", "prune", "decompress", "wgrad", "block_sumsq", "num_blocks", "keep_count",
+__all__ = ["BSR", "BsrError", "prune", "prune_stochastic", "decompress", "wgrad", "block_sumsq", "num_blocks", "keep_count",
            "storage_bytes", "workspace", "version", "set_pdl", "wgrad_multicast", "affine_wgrad", "SparseAffine", "SparseLinear", "sparse_linear", "prune_global",
            "RowBSR", "prune_rows", "decompress_rows", "wgrad_rows", "act_prune"]
 
@@ -167,6 +167,33 @@ def prune(X: torch.Tensor, b: int, keep: float | None = None, k: int | None = No
     cs = out.c_struct()
     _lib.check(lib.bsr_prune_k(X.data_ptr(), M, K, b, k, _dt(X), ctypes.byref(cs), ws.data_ptr(), ws.numel(),
                                _stream(stream)))
+    return out
+
+
+def prune_stochastic(X: torch.Tensor, b: int, keep: float | None = None, k: int | None = None, window: int = 0,
+                     p: float = 0.5, seed: int = 0, out: BSR | None = None, stream=None) -> BSR:
+    """Top-k with stochastic boundary swapping (DESIGN reading R19):
+    pair i < min(window, k, N-k) of (rank k-1-i, rank k+i) swaps kept/pruned iff
+    the counter-based uniform u_i(seed) < p.  Exactly k blocks kept; same seed,
+    same selection."""
+    lib = _lib.load()
+    X = _cuda2d(X, "X")
+    M, K = X.shape
+    N = num_blocks(M, K, b)
+    if N < 0:
+        raise _lib.BsrError(2, f"b={b} must divide M={M} and K={K}")
+    if (keep is None) == (k is None):
+        raise ValueError("give exactly one of keep or k")
+    if k is None:
+        k = keep_count(N, keep)
+    if out is None:
+        out = alloc_bsr(M, K, b, k, X.dtype, X.device)
+    else:
+        _check_out_bsr(out, M, K, b, k, X.dtype, X.device)
+    ws = workspace(lib.bsr_prune_stochastic_workspace_bytes(M, K, b), X.device, kind="prune", stream=stream)
+    cs = out.c_struct()
+    _lib.check(lib.bsr_prune_stochastic(X.data_ptr(), M, K, b, k, int(window), float(p), int(seed) & (2**64 - 1),
+                                        _dt(X), ctypes.byref(cs), ws.data_ptr(), ws.numel(), _stream(stream)))
     return out
 
 

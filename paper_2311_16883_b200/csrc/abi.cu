@@ -214,6 +214,51 @@ bsr_status_t bsr_prune_k(const void *X, int64_t M, int64_t K, int32_t b, int64_t
     return prune_impl(X, M, K, b, k, dtype, out, ws, ws_bytes, stream);
 }
 
+size_t bsr_prune_stochastic_workspace_bytes(int64_t M, int64_t K, int32_t b) {
+    const int64_t N = bsr_num_blocks(M, K, b);
+    if (N < 0 || !supported_b(b)) return 0;
+    return bsrp::stoch_ws_layout(N).total;
+}
+
+bsr_status_t bsr_prune_stochastic(const void *X, int64_t M, int64_t K, int32_t b, int64_t k, int64_t window,
+                                  double p, uint64_t seed, int32_t dtype, bsr_t *out, void *ws, size_t ws_bytes,
+                                  void *stream) {
+    bsr_status_t st = check_shape(M, K, b, dtype);
+    if (st != BSR_OK) return st;
+    const int64_t N = (M / b) * (K / b);
+    if (window < 0) return fail(BSR_ERR_INVALID_ARG, "window=%lld is negative", (long long)window);
+    if (!(p >= 0.0 && p <= 1.0)) return fail(BSR_ERR_INVALID_ARG, "p=%g must be in [0, 1]", p);
+    if (k < 0 || k > N) return fail(BSR_ERR_INVALID_ARG, "k=%lld outside [0, N=%lld]", (long long)k, (long long)N);
+    const int64_t w = std::min<int64_t>(window, std::min<int64_t>(k, N - k));
+    if (w > bsrp::kStochMaxWindow)
+        return fail(BSR_ERR_INVALID_ARG, "window: min(window, k, N-k)=%lld exceeds %d", (long long)w,
+                    bsrp::kStochMaxWindow);
+    if (w == 0) return prune_impl(X, M, K, b, k, dtype, out, ws, ws_bytes, stream);
+    if (!X) return fail(BSR_ERR_INVALID_ARG, "X is NULL");
+    if (!out || !out->rowptr || !out->colidx || !out->values)
+        return fail(BSR_ERR_INVALID_ARG, "output BSR descriptor or one of its arrays is NULL");
+    if (!aligned16(X)) return fail(BSR_ERR_ALIGNMENT, "X is not 16-byte aligned");
+    if (!aligned16(out->values)) return fail(BSR_ERR_ALIGNMENT, "out->values is not 16-byte aligned");
+    const int es = elem_size(dtype);
+    const size_t xbytes = (size_t)M * K * es;
+    if (overlap(X, xbytes, out->values, (size_t)k * b * b * es) || overlap(X, xbytes, out->colidx, (size_t)k * 4) ||
+        overlap(X, xbytes, out->rowptr, (size_t)(M / b + 1) * 4))
+        return fail(BSR_ERR_INVALID_ARG, "X overlaps an output array");
+    const size_t need = bsrp::stoch_ws_layout(N).total;
+    if (!ws || ws_bytes < need)
+        return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
+    if (!aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
+    cudaError_t e = bsrp::launch_prune_stochastic(X, M, K, b, es, k, window, p, seed, out->rowptr, out->colidx,
+                                                  out->values, ws, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_status(e, "bsr_prune_stochastic launch");
+    out->M = M;
+    out->K = K;
+    out->b = b;
+    out->dtype = dtype;
+    out->nnzb = k;
+    return ok();
+}
+
 bsr_status_t bsr_block_sumsq(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype, float *sumsq,
                              void *stream) {
     bsr_status_t st = check_shape(M, K, b, dtype);

@@ -39,10 +39,21 @@ cudaError_t launch_pdl(bool on, void (*kern)(KArgs...), dim3 grid, dim3 block, s
 
 // Workspace layout of bsr_prune (byte offsets; all 256-aligned).
 struct PruneWs {
-    size_t hdr, hist1, hist2, hist3, cta_cnt, sumsq, slot, cand, total, zero_bytes;
+    size_t hdr, hist1, hist2, hist3, sstate, shist, cta_cnt, sumsq, slot, cand, total, zero_bytes;
 };
 constexpr int kMaxGrid = 2048;
 PruneWs prune_ws_layout(int64_t N);
+// bsr_prune_stochastic: the bsr_prune layout followed by the selection state,
+// the refinement histograms, per-CTA tie counts and the boundary list.
+constexpr int kStochMaxWindow = 4096;  // boundary pairs (the 2w boundary blocks are sorted in one CTA)
+struct StochWs {
+    PruneWs base;
+    size_t state, shist, cta2, blist, total;
+};
+StochWs stoch_ws_layout(int64_t N);
+cudaError_t launch_prune_stochastic(const void *X, int64_t M, int64_t K, int b, int es, int64_t k, int64_t window,
+                                    double prob, uint64_t seed, int32_t *rowptr, int32_t *colidx, void *values,
+                                    void *ws, cudaStream_t stream);
 
 // Returns cudaSuccess or the launch error.
 cudaError_t launch_prune(const void *X, int64_t M, int64_t K, int b, int es, int64_t k,

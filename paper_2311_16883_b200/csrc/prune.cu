@@ -920,6 +920,8 @@ PruneWs prune_ws_layout(int64_t N) {
     w.hist1 = o;    o += align256(kH1 * 4);
     w.hist2 = o;    o += align256(kH2 * 4);
     w.hist3 = o;    o += align256(kH3 * 4);
+    w.sstate = o;   o += align256(2 * 8 * 4 + 4);  // bsr_prune_stochastic: [2][ST_WORDS] + boundary counter
+    w.shist = o;    o += align256(2 * kH2 * 4);    // bsr_prune_stochastic: refinement histograms
     w.zero_bytes = o;
     w.cta_cnt = o;  o += align256(2 * kMaxGrid * 4);
     w.sumsq = o;    o += align256((size_t)N * 4);
@@ -1115,6 +1117,399 @@ cudaError_t launch_prune_threshold(const void *X, int64_t M, int64_t K, int b, i
         return cudaLaunchCooperativeKernel((const void *)prune_apply_kernel<ES_, B_>, dim3((unsigned)grid),      \
                                            dim3(kThreads), args, 0, stream);                                    \
     }())
+    if (es == 4) {
+        BSRP_DISPATCH_B(4, b, CALL)
+    } else {
+        BSRP_DISPATCH_B(2, b, CALL)
+    }
+#undef CALL
+}
+
+// ---- stochastic boundary swapping (DESIGN reading R19) --------
+// "randomly swapping blocks near the top-k threshold, resulting in some blocks
+// above the threshold being pruned anyway, and vice-versa below threshold"
+// (P:L661-666).  Ranks follow the deterministic order (key desc, flat index asc);
+// with A = k - w and B = k + w (w = min(window, k, N - k) > 0):
+//   ranks [0, A)      kept,
+//   ranks [A, B)      the boundary: pair i (rank k-1-i, rank k+i) swaps iff
+//                     u_i < p, u_i = splitmix64(seed, i) as a 53-bit uniform,
+//   ranks [B, N)      pruned.
+// Kernels (stream order, 9 launches, graph-capturable):
+//   prune_sums_kernel  block sums + digit-0 histogram (shared with bsr_prune)
+//   stoch_update x3 / stoch_hist x2   radix select of ranks A and B together
+//   stoch_mark (coop)  flat-order tie scan: slot[f] = 1 for ranks < A, the
+//                      2w boundary blocks appended as (key, flat index)
+//   stoch_swap (1 CTA) bitonic sort of the boundary by rank, the swaps
+//   stoch_pack (coop)  flat-order scan of the final marks, rowptr/colidx, copy
+enum { ST_T = 0, ST_SHIFT = 1, ST_R = 2, ST_ABOVE = 3, ST_DONE = 4, ST_TGT = 5, ST_WORDS = 8 };
+
+StochWs stoch_ws_layout(int64_t N) {
+    StochWs w;
+    w.base = prune_ws_layout(N);
+    size_t o = w.base.total;
+    w.cta2 = o;   o += align256(2 * kMaxGrid * 4);
+    w.blist = o;  o += align256(2 * kStochMaxWindow * 8);
+    w.total = o;
+    return w;
+}
+
+__device__ __forceinline__ double swap_uniform(uint64_t seed, uint64_t i) {
+    uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// One CTA: resolve the next key digit of both selections (targets A, B) from the
+// histogram, then zero the histogram (self-cleaning workspace).
+__global__ void __launch_bounds__(kThreads) stoch_update_kernel(int level, uint32_t *hist, uint32_t *st,
+                                                                int64_t tA, int64_t tB) {
+    __shared__ uint64_t s_warp[32];
+    __shared__ uint32_t s_sel[4];
+    const int nb = level == 0 ? kH1 : level == 1 ? kH2 : kH3;
+    const int w = level == 0 ? 12 : level == 1 ? 10 : 9;
+    for (int t = 0; t < 2; ++t) {
+        uint32_t *S = st + t * ST_WORDS;
+        if (level == 0) {
+            const uint32_t tgt = (uint32_t)(t == 0 ? tA : tB);
+            if (tgt == 0) {  // empty selection: a prefix no key reaches, no ties
+                if (threadIdx.x == 0) {
+                    S[ST_T] = 0xffffffffu; S[ST_SHIFT] = 0; S[ST_R] = 0; S[ST_ABOVE] = 0; S[ST_DONE] = 1;
+                    S[ST_TGT] = 0;
+                }
+                continue;
+            }
+            select_bin(hist, nb, tgt, s_warp, s_sel);
+            if (threadIdx.x == 0) {
+                S[ST_T] = s_sel[0]; S[ST_SHIFT] = 19; S[ST_ABOVE] = s_sel[1]; S[ST_R] = tgt - s_sel[1];
+                S[ST_DONE] = tgt - s_sel[1] >= s_sel[2];
+                S[ST_TGT] = tgt;
+            }
+        } else {
+            const uint32_t done = __ldcg(S + ST_DONE), r = __ldcg(S + ST_R);
+            if (done) continue;
+            select_bin(hist + t * kH2, nb, r, s_warp, s_sel);
+            if (threadIdx.x == 0) {
+                const uint32_t above = S[ST_ABOVE] + s_sel[1];
+                S[ST_T] = (S[ST_T] << w) | s_sel[0];
+                S[ST_SHIFT] -= w;
+                S[ST_ABOVE] = above;
+                S[ST_R] = S[ST_TGT] - above;
+                S[ST_DONE] = (S[ST_TGT] - above >= s_sel[2]) || level == 2;
+            }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    const int nz = level == 0 ? kH1 : 2 * kH2;
+    for (int i = threadIdx.x; i < nz; i += kThreads) hist[i] = 0;
+}
+
+// Histogram of the next digit of the keys matching each unresolved selection's prefix.
+__global__ void __launch_bounds__(kThreads) stoch_hist_kernel(int level, const float *__restrict__ sumsq, int64_t N,
+                                                              const uint32_t *__restrict__ st, uint32_t *hist) {
+    __shared__ uint32_t s_h[2][kH2];
+    const int nb = level == 1 ? kH2 : kH3, nshift = level == 1 ? 9 : 0;
+    const int lane = threadIdx.x & 31;
+    bool act[2];
+    uint32_t T[2], sh[2];
+    for (int t = 0; t < 2; ++t) {
+        act[t] = st[t * ST_WORDS + ST_DONE] == 0;
+        T[t] = st[t * ST_WORDS + ST_T];
+        sh[t] = st[t * ST_WORDS + ST_SHIFT];
+    }
+    for (int i = threadIdx.x; i < 2 * kH2; i += kThreads) (&s_h[0][0])[i] = 0;
+    __syncthreads();
+    if (act[0] || act[1])
+        for (int64_t fb = (int64_t)blockIdx.x * kThreads; fb < N; fb += (int64_t)gridDim.x * kThreads) {
+            const int64_t f = fb + threadIdx.x;
+            const uint32_t key = f < N ? key_of(__ldcg(sumsq + f)) : 0u;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const bool in = act[t] && f < N && (key >> sh[t]) == T[t];
+                const uint32_t bin = (key >> nshift) & (uint32_t)(nb - 1);
+                const uint32_t im = __ballot_sync(0xffffffffu, in);
+                if (!im) continue;
+                const int l0 = __ffs(im) - 1;
+                const uint32_t b0 = __shfl_sync(0xffffffffu, bin, l0);
+                if (__all_sync(0xffffffffu, !in || bin == b0)) {  // a warp of ties adds once
+                    if (lane == l0) atomicAdd(&s_h[t][b0], (uint32_t)__popc(im));
+                } else if (in) {
+                    atomicAdd(&s_h[t][bin], 1u);
+                }
+            }
+        }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * kH2; i += kThreads) {
+        const uint32_t v = (&s_h[0][0])[i];
+        if (v) atomicAdd(hist + i, v);
+    }
+}
+
+struct StochParams {
+    const float *sumsq;
+    int64_t N;
+    int32_t *slot;           // out: 1 for ranks < A, else 0
+    const uint32_t *st;
+    uint32_t *bar, *cta2;
+    uint32_t *bcount, *shist;
+    unsigned long long *blist;  // (key << 32) | (0xffffffff - f): descending order = rank order
+};
+
+// Cooperative: per-CTA tie counts of both selections, grid barrier, flat-order
+// scan (the same tie rule as scan_and_index: the first r ties in flat order).
+__global__ void __launch_bounds__(kThreads) stoch_mark_kernel(StochParams q) {
+    __shared__ uint64_t s_warp[32];
+    __shared__ uint32_t s_flag;
+    const int lane = threadIdx.x & 31;
+    const int64_t f0 = (int64_t)blockIdx.x * q.N / gridDim.x, f1 = (int64_t)(blockIdx.x + 1) * q.N / gridDim.x;
+    const uint32_t TA = q.st[ST_T], shA = q.st[ST_SHIFT], rA = q.st[ST_R];
+    const uint32_t TB = q.st[ST_WORDS + ST_T], shB = q.st[ST_WORDS + ST_SHIFT], rB = q.st[ST_WORDS + ST_R];
+    uint32_t ta = 0, tb = 0;
+    for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) {
+        const uint32_t key = key_of(q.sumsq[f]);
+        ta += (key >> shA) == TA;
+        tb += (key >> shB) == TB;
+    }
+    {
+        uint64_t tot;
+        block_excl_scan(((uint64_t)ta << 32) | tb, s_warp, tot);
+        if (threadIdx.x == 0) {
+            q.cta2[2 * blockIdx.x] = (uint32_t)(tot >> 32);
+            q.cta2[2 * blockIdx.x + 1] = (uint32_t)tot;
+        }
+    }
+    grid_barrier(q.bar, 0);
+    uint64_t pre = 0;
+    for (int c = threadIdx.x; c < (int)blockIdx.x; c += kThreads)
+        pre += ((uint64_t)__ldcg(q.cta2 + 2 * c) << 32) | __ldcg(q.cta2 + 2 * c + 1);
+    {
+        uint64_t tot;
+        block_excl_scan(pre, s_warp, tot);
+        pre = tot;
+    }
+    if (threadIdx.x == 0) {  // self-cleaning barrier counter (see prune_apply_kernel)
+        __threadfence();
+        s_flag = atomicAdd(q.bar + 32, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_flag && threadIdx.x == 0) {
+        __threadfence();
+        q.bar[0] = 0;
+        q.bar[32] = 0;
+    }
+    uint32_t baseA = (uint32_t)(pre >> 32), baseB = (uint32_t)pre;
+    for (int64_t fb = f0; fb < f1; fb += kThreads) {
+        const int64_t f = fb + threadIdx.x;
+        const bool in = f < f1;
+        const uint32_t key = in ? key_of(q.sumsq[f]) : 0u;
+        const uint32_t kA = key >> shA, kB = key >> shB;
+        const uint32_t tA = in && kA == TA, tB = in && kB == TB;
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan(((uint64_t)tA << 32) | tB, s_warp, tot);
+        const uint32_t bA = baseA + (uint32_t)(ex >> 32), bB = baseB + (uint32_t)ex;
+        const bool inA = in && (kA > TA || (tA && bA < rA));
+        const bool inB = in && (kB > TB || (tB && bB < rB));
+        const bool bnd = inB && !inA;
+        if (in) q.slot[f] = inA ? 1 : 0;
+        const uint32_t m = __ballot_sync(0xffffffffu, bnd);
+        uint32_t pos = 0;
+        if (m && lane == 0) pos = atomicAdd(q.bcount, (uint32_t)__popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << lane) - 1u));
+        if (bnd) {
+            if (pos >= 2u * kStochMaxWindow) __trap();  // cannot happen: |ranks [A, B)| = 2w
+            q.blist[pos] = ((unsigned long long)key << 32) | (0xffffffffu - (uint32_t)f);
+        }
+        baseA += (uint32_t)(tot >> 32);
+        baseB += (uint32_t)tot;
+    }
+}
+
+// One CTA: sort the 2w boundary blocks by rank (bitonic, descending composite
+// key), apply the swaps, mark the kept ones, reset the boundary counter.
+__global__ void __launch_bounds__(1024) stoch_swap_kernel(unsigned long long *__restrict__ blist, uint32_t *bcount,
+                                                          int32_t *__restrict__ slot, int w, double prob,
+                                                          unsigned long long seed) {
+    extern __shared__ unsigned long long s_b[];
+    const int n = 2 * w;
+    if (threadIdx.x == 0 && __ldcg(bcount) != (uint32_t)n) __trap();  // workspace not zero-filled
+    int P = 1;
+    while (P < n) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) s_b[i] = i < n ? __ldcg(blist + i) : 0ull;
+    __syncthreads();
+    if (threadIdx.x == 0) *bcount = 0;
+    for (int kk = 2; kk <= P; kk <<= 1)
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long a = s_b[i], b2 = s_b[ixj];
+                    const bool desc = (i & kk) == 0;
+                    if (desc ? a < b2 : a > b2) {
+                        s_b[i] = b2;
+                        s_b[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    // sorted position j holds rank A + j: j < w is kept unless pair w-1-j swaps,
+    // j >= w is kept iff pair j-w swaps
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const int i = j < w ? w - 1 - j : j - w;
+        const bool swapped = swap_uniform(seed, (uint64_t)i) < prob;
+        const bool keep = j < w ? !swapped : swapped;
+        const uint32_t f = 0xffffffffu - (uint32_t)(s_b[j] & 0xffffffffull);
+        if (keep) slot[f] = 1;
+    }
+}
+
+// Cooperative: output slots of the marked blocks in flat order, rowptr, colidx, copy.
+template <int ES, int B>
+__global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) stoch_pack_kernel(PruneParams p) {
+    using G_ = Geo<ES, B>;
+    __shared__ uint64_t s_warp[32];
+    __shared__ uint32_t s_flag;
+    const int64_t u0 = (int64_t)blockIdx.x * p.units / gridDim.x;
+    const int64_t u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
+    auto flat_start = [&](int64_t u) -> int64_t {
+        return u >= p.units ? p.N : (u / p.upr) * p.nbc + (u % p.upr) * G_::G;
+    };
+    const int64_t f0 = flat_start(u0), f1 = flat_start(u1);
+    uint32_t nk = 0;
+    for (int64_t f = f0 + threadIdx.x; f < f1; f += kThreads) nk += p.slot[f] == 1;
+    {
+        uint64_t tot;
+        block_excl_scan(nk, s_warp, tot);
+        if (threadIdx.x == 0) p.cta_cnt[blockIdx.x] = (uint32_t)tot;
+    }
+    grid_barrier(p.bar, 0);
+    uint64_t pre = 0;
+    for (int c = threadIdx.x; c < (int)blockIdx.x; c += kThreads) pre += __ldcg(p.cta_cnt + c);
+    {
+        uint64_t tot;
+        block_excl_scan(pre, s_warp, tot);
+        pre = tot;
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_flag = atomicAdd(p.bar + 32, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_flag && threadIdx.x == 0) {
+        __threadfence();
+        p.bar[0] = 0;
+        p.bar[32] = 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.rowptr[0] = 0;
+    uint32_t base = (uint32_t)pre;
+    for (int64_t fb = f0; fb < f1; fb += kThreads) {
+        const int64_t f = fb + threadIdx.x;
+        const bool in = f < f1;
+        const uint32_t kp = in && p.slot[f] == 1;
+        uint64_t tot;
+        const uint32_t pos = base + (uint32_t)block_excl_scan(kp, s_warp, tot);
+        if (in) {
+            const bool kept = kp && pos < (uint64_t)p.k;
+            const int64_t I = f / p.nbc, J = f - I * p.nbc;
+            p.slot[f] = kept ? (int32_t)pos : -1;
+            if (kept) p.colidx[pos] = (int32_t)J;
+            if (J == p.nbc - 1) p.rowptr[I + 1] = (int32_t)(pos + kp);
+        }
+        base += (uint32_t)tot;
+    }
+    __syncthreads();
+    pack_kept<ES, B>(p, u0, u1);
+}
+
+template <int ES, int B>
+static cudaError_t launch_stoch_t(PruneParams p, StochParams q, int64_t wn, double prob,
+                                  uint64_t seed, cudaStream_t stream) {
+    const int sms = num_sms();
+    const int64_t per = kThreads / 32;
+    const int64_t sgrid = std::max<int64_t>(1, std::min<int64_t>((p.units + per - 1) / per, (int64_t)sms));
+    cudaError_t e = launch_pdl(false, prune_sums_kernel<ES, B>, dim3((unsigned)sgrid), dim3(kThreads), 0, stream, p);
+    if (e != cudaSuccess) return e;
+    uint32_t *st = const_cast<uint32_t *>(q.st);
+    uint32_t *shist = q.shist;
+    const int64_t tA = p.k - wn, tB = p.k + wn;
+    const int64_t hgrid = std::max<int64_t>(1, std::min<int64_t>((p.N + kThreads - 1) / kThreads, 2 * (int64_t)sms));
+    stoch_update_kernel<<<1, kThreads, 0, stream>>>(0, p.hist1, st, tA, tB);
+    for (int level = 1; level <= 2; ++level) {
+        stoch_hist_kernel<<<(unsigned)hgrid, kThreads, 0, stream>>>(level, p.sumsq, p.N, q.st, shist);
+        stoch_update_kernel<<<1, kThreads, 0, stream>>>(level, shist, st, tA, tB);
+    }
+    count_launch(6);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stoch_mark_kernel, kThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorLaunchOutOfResources;
+    int64_t mgrid = std::min<int64_t>((int64_t)occ * sms, kMaxGrid);
+    mgrid = std::min<int64_t>(mgrid, std::max<int64_t>(1, (p.N + kThreads - 1) / kThreads));
+    {
+        void *args[] = {&q};
+        e = cudaLaunchCooperativeKernel((const void *)stoch_mark_kernel, dim3((unsigned)mgrid), dim3(kThreads), args, 0,
+                                        stream);
+        count_launch();
+        if (e != cudaSuccess) return e;
+    }
+    int P = 1;
+    while (P < 2 * wn) P <<= 1;
+    const size_t smem = (size_t)P * 8;
+    e = cudaFuncSetAttribute(stoch_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    stoch_swap_kernel<<<1, 1024, smem, stream>>>(q.blist, q.bcount, p.slot, (int)wn, prob, (unsigned long long)seed);
+    count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stoch_pack_kernel<ES, B>, kThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorLaunchOutOfResources;
+    int64_t pgrid = std::min<int64_t>((int64_t)occ * sms, kMaxGrid);
+    pgrid = std::min<int64_t>(pgrid, std::max<int64_t>(1, (p.units + per - 1) / per));
+    void *args[] = {&p};
+    count_launch();
+    return cudaLaunchCooperativeKernel((const void *)stoch_pack_kernel<ES, B>, dim3((unsigned)pgrid), dim3(kThreads),
+                                       args, 0, stream);
+}
+
+cudaError_t launch_prune_stochastic(const void *X, int64_t M, int64_t K, int b, int es, int64_t k, int64_t window,
+                                    double prob, uint64_t seed, int32_t *rowptr, int32_t *colidx, void *values,
+                                    void *ws, cudaStream_t stream) {
+    const int64_t N = (M / b) * (K / b);
+    const int64_t wn = std::min<int64_t>(window, std::min<int64_t>(k, N - k));
+    if (wn <= 0) return launch_prune(X, M, K, b, es, k, rowptr, colidx, values, ws, stream, 0);
+    if (wn > kStochMaxWindow) return cudaErrorInvalidValue;
+    const StochWs w = stoch_ws_layout(N);
+    char *base = static_cast<char *>(ws);
+    PruneParams p{};
+    p.X = X;
+    p.K = K;
+    p.nbr = M / b;
+    p.nbc = K / b;
+    p.N = N;
+    p.k = k;
+    p.rowptr = rowptr;
+    p.colidx = colidx;
+    p.values = values;
+    p.bar = reinterpret_cast<uint32_t *>(base + w.base.hdr);
+    p.hist1 = reinterpret_cast<uint32_t *>(base + w.base.hist1);
+    p.cta_cnt = reinterpret_cast<uint32_t *>(base + w.base.cta_cnt);
+    p.sumsq = reinterpret_cast<float *>(base + w.base.sumsq);
+    p.slot = reinterpret_cast<int32_t *>(base + w.base.slot);
+    StochParams q{};
+    q.sumsq = p.sumsq;
+    q.N = N;
+    q.slot = p.slot;
+    q.st = reinterpret_cast<uint32_t *>(base + w.base.sstate);
+    q.bcount = reinterpret_cast<uint32_t *>(base + w.base.sstate) + 2 * ST_WORDS;
+    q.bar = p.bar;
+    q.cta2 = reinterpret_cast<uint32_t *>(base + w.cta2);
+    q.blist = reinterpret_cast<unsigned long long *>(base + w.blist);
+    q.shist = reinterpret_cast<uint32_t *>(base + w.base.shist);
+#define CALL(ES_, B_) (p.upr = units_per_row<ES_, B_>(p.nbc), p.units = p.nbr * p.upr, \
+                       launch_stoch_t<ES_, B_>(p, q, wn, prob, seed, stream))
     if (es == 4) {
         BSRP_DISPATCH_B(4, b, CALL)
     } else {
