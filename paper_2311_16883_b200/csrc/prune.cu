@@ -180,7 +180,8 @@ __device__ __forceinline__ void select_bin(const uint32_t *hist, int nbins, uint
 // (above, tie) counts of every block before it (`pre`): output slots,
 // colidx and rowptr, slot[f] = -1 for pruned blocks.
 __device__ __forceinline__ void scan_and_index(const PruneParams &p, int64_t f0, int64_t f1, uint64_t pre,
-                                               uint32_t prefix, int shift, uint32_t r, uint64_t *s_warp) {
+                                               uint32_t prefix, int shift, uint32_t r, uint64_t *s_warp,
+                                               const uint32_t *s_keys = nullptr) {
     uint32_t base_a = (uint32_t)(pre >> 32), base_t = (uint32_t)pre;
     if (blockIdx.x == 0 && threadIdx.x == 0) p.rowptr[0] = 0;
     for (int64_t fb = f0; fb < f1; fb += kThreads) {
@@ -188,7 +189,7 @@ __device__ __forceinline__ void scan_and_index(const PruneParams &p, int64_t f0,
         const bool in = f < f1;
         uint32_t a = 0, t = 0;
         if (in) {
-            uint32_t kk = key_of(p.sumsq[f]) >> shift;
+            uint32_t kk = (s_keys ? s_keys[f] : key_of(p.sumsq[f])) >> shift;
             a = kk > prefix;
             t = kk == prefix;
         }
@@ -478,17 +479,23 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_kernel(Prun
 // Two plain (non-cooperative) launches chained with programmatic dependent
 // launch instead of one cooperative kernel with grid barriers, for N <= kSmallN
 // keys (S12 fc1/fc2 at b >= 16-32, B24 per-rank fc1): the kernel boundary is the
-// only grid-wide synchronisation, and PDL hides each launch behind its
-// predecessor's tail.
+// only grid-wide synchronisation.
 //   prune_sums_kernel : phase 1 of prune_kernel (same units, same reduction tree,
-//                       so bit-identical block sums) + the level-1 histogram.
-//   prune_finish_kernel: every CTA loads the global histogram and ALL N keys into
-//                       shared memory, resolves the exact threshold (the
-//                       boundary bin refined by two more digits over the keys in
-//                       shared memory -- no candidate list, no overflow case),
-//                       counts the (above, tie) keys before its own flat range
-//                       from shared memory, then scans and packs its range as
-//                       prune_kernel does.  No grid barrier.
+//                       so bit-identical block sums).  It triggers its dependent
+//                       at its start, so the finishing CTAs are already resident
+//                       (waiting in griddepcontrol.wait) when the sums complete.
+//   prune_finish_kernel: every CTA loads ALL N keys into shared memory and counts
+//                       their first digit there (no global histogram, nothing to
+//                       clean up), resolves the exact threshold (the boundary bin
+//                       refined by two more digits over a candidate list in shared
+//                       memory), counts the (above, tie) keys before its own flat
+//                       range, then scans and packs its range as prune_kernel does.
+//                       No grid barrier, no global atomics.
+//   STOCH (bsr_prune_stochastic, R19): every CTA also resolves ranks k - w and
+//                       k + w, walks all keys in flat order to mark ranks < k - w
+//                       and collect the 2w boundary blocks, sorts them by rank in
+//                       shared memory and applies the swaps -- each CTA reaches the
+//                       same kept set and packs its own range.
 constexpr int64_t kSmallN = 24576;  // keys held in shared memory by every finishing CTA (96 KB); measured:
                                     // at 37632 keys (S12 fc1 b = 16) the per-CTA passes cost more than the
                                     // cooperative kernel's barriers
@@ -500,12 +507,17 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_sums_kernel
     __shared__ uint32_t s_hist[kH1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kThreads / 32;
     const int j = lane / G_::LPB, sub = lane % G_::LPB;
-    for (int i = threadIdx.x; i < kH1; i += kThreads) s_hist[i] = 0;
-    __syncthreads();
+    const bool hist = p.hist1 != nullptr;  // global first-digit histogram (the multi-kernel stochastic path)
+    if (hist) {
+        for (int i = threadIdx.x; i < kH1; i += kThreads) s_hist[i] = 0;
+        __syncthreads();
+    }
     pdl_wait();  // launched with PDL: the predecessor (e.g. the previous step) has completed
+    pdl_trigger();  // the finishing kernel may become resident now; it waits for this grid's completion
     if (p.presummed) {
-        for (int64_t f = (int64_t)blockIdx.x * kThreads + threadIdx.x; f < p.N; f += (int64_t)gridDim.x * kThreads)
-            atomicAdd(&s_hist[key_of(p.sumsq[f]) >> 19], 1u);
+        if (hist)
+            for (int64_t f = (int64_t)blockIdx.x * kThreads + threadIdx.x; f < p.N; f += (int64_t)gridDim.x * kThreads)
+                atomicAdd(&s_hist[key_of(p.sumsq[f]) >> 19], 1u);
     } else {
         for (int64_t u = (int64_t)blockIdx.x * nw + wid; u < p.units; u += (int64_t)gridDim.x * nw) {
             const int64_t I = u / p.upr, J = (u % p.upr) * G_::G + j;
@@ -513,99 +525,37 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) prune_sums_kernel
             const float sq = block_sumsq_warp<ES, B>(p.X, p.K, I, J, sub, valid);
             if (valid && sub == 0) {
                 p.sumsq[I * p.nbc + J] = sq;
-                atomicAdd(&s_hist[key_of(sq) >> 19], 1u);
+                if (hist) atomicAdd(&s_hist[key_of(sq) >> 19], 1u);
             }
         }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kH1; i += kThreads)
-        if (s_hist[i]) atomicAdd(p.hist1 + i, s_hist[i]);
-    pdl_trigger();  // the finishing kernel may become resident; it waits for this grid's completion
+    if (hist) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < kH1; i += kThreads)
+            if (s_hist[i]) atomicAdd(p.hist1 + i, s_hist[i]);
+    }
 }
 
-template <int ES, int B>
-__global__ void __launch_bounds__(kThreads, 1) prune_finish_kernel(PruneParams p) {
-    extern __shared__ uint32_t s_key[];  // [N] key bits, flat order; then the candidate list
-    __shared__ uint32_t s_h2[1024];
-    __shared__ uint64_t s_warp[32];
-    __shared__ uint32_t s_sel[4];
-    using G_ = Geo<ES, B>;
+// Shared-memory histogram add with the warp's ties folded into one atomic
+// (all lanes of the warp must call it).
+__device__ __forceinline__ void hist_add_warp(uint32_t *h, uint32_t bin, bool valid) {
     const int lane = threadIdx.x & 31;
-    const int64_t u0 = (int64_t)blockIdx.x * p.units / gridDim.x;
-    const int64_t u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
-    auto flat_start = [&](int64_t u) -> int64_t {
-        return u >= p.units ? p.N : (u / p.upr) * p.nbc + (u % p.upr) * G_::G;
-    };
-    const int64_t f0 = flat_start(u0), f1 = flat_start(u1);
-    const int N = (int)p.N;
-    uint32_t *s_ck = s_key + ((N + 3) & ~3);  // [kSmallCand] candidate keys
-    uint32_t *s_cf = s_ck + kSmallCand;       // [kSmallCand] their flat indices
-    pdl_wait();  // the sums kernel has completed: sumsq and hist1 are final
-    // boundary bin of the first digit from the global histogram
-    const uint32_t k = (uint32_t)p.k;
-    select_bin(p.hist1, kH1, k, s_warp, s_sel);
-    uint32_t prefix = s_sel[0], above = s_sel[1], bincnt = s_sel[2];
-    // every key into shared memory (16-byte loads, several in flight per thread)
-    {
-        const float4 *src = reinterpret_cast<const float4 *>(p.sumsq);
-        const int n4 = N / 4;
-        for (int i0 = threadIdx.x; i0 < n4; i0 += 4 * kThreads) {
-            float4 v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = i0 + u * kThreads < n4 ? __ldcg(src + i0 + u * kThreads) : float4{};
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (i0 + u * kThreads < n4)
-                    reinterpret_cast<uint4 *>(s_key)[i0 + u * kThreads] =
-                        make_uint4(key_of(v[u].x), key_of(v[u].y), key_of(v[u].z), key_of(v[u].w));
-        }
-        for (int f = n4 * 4 + threadIdx.x; f < N; f += kThreads) s_key[f] = key_of(__ldcg(p.sumsq + f));
+    const uint32_t m = __ballot_sync(0xffffffffu, valid);
+    if (!m) return;
+    const int l0 = __ffs(m) - 1;
+    const uint32_t b0 = __shfl_sync(0xffffffffu, bin, l0);
+    if (__all_sync(0xffffffffu, !valid || bin == b0)) {
+        if (lane == l0) atomicAdd(&h[b0], (uint32_t)__popc(m));
+    } else if (valid) {
+        atomicAdd(&h[bin], 1u);
     }
-    // self-cleaning workspace: this CTA is done with hist1; the last one zeroes it
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_sel[3] = atomicAdd(p.bar + 32, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_sel[3]) {
-        __threadfence();
-        for (int i = threadIdx.x; i < kH1; i += kThreads) p.hist1[i] = 0;
-        if (threadIdx.x == 0) p.bar[32] = 0;
-    }
-    // Refine the boundary bin (bits 18..9, then 8..0).  Its keys are first compacted
-    // into a candidate list (key, flat index) in shared memory, so the two
-    // histogram passes and the prefix count run over the candidates only; a bin
-    // too large for the list (heavy ties) is refined over all keys instead.
-    const uint32_t prefix1 = prefix;
-    int shift = 19;
-    uint32_t r = k - above;
-    uint32_t nc = 0;
-    const bool refine = r < bincnt;
-    const bool use_cand = refine && bincnt <= (uint32_t)kSmallCand;
-    if (use_cand) {
-        __syncthreads();  // every thread has read the clean-up flag in s_sel[3]
-        if (threadIdx.x == 0) s_sel[3] = 0;
-        __syncthreads();
-        for (int fb = 0; fb < N; fb += kThreads) {
-            const int f = fb + threadIdx.x;
-            const bool in = f < N && (s_key[f] >> 19) == prefix1;
-            const uint32_t m = __ballot_sync(0xffffffffu, in);
-            uint32_t base = 0;
-            if (m && lane == 0) base = atomicAdd(&s_sel[3], (uint32_t)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (in) {
-                const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
-                s_ck[pos] = s_key[f];
-                s_cf[pos] = (uint32_t)f;
-            }
-        }
-        __syncthreads();
-        nc = s_sel[3];  // == bincnt
-        __syncthreads();
-    }
-    const uint32_t *arr = use_cand ? s_ck : s_key;
-    const int len = use_cand ? (int)nc : N;
+}
+
+// Refine a boundary bin (prefix at `shift`) by the next digits until the target's
+// tie quota r is resolved or the key is exact.  arr/len: keys to histogram.
+__device__ __forceinline__ void refine_bin(const uint32_t *arr, int len, uint32_t target, uint32_t &prefix, int &shift,
+                                           uint32_t &above, uint32_t &bincnt, uint32_t &r, uint32_t *s_h2,
+                                           uint64_t *s_warp, uint32_t *s_sel) {
     for (int pass = 0; pass < 2 && r < bincnt; ++pass) {
         const int w = pass == 0 ? 10 : 9;
         const int nshift = shift - w;
@@ -615,16 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1) prune_finish_kernel(PruneParams p
             const int f = fb + threadIdx.x;
             const uint32_t key = f < len ? arr[f] : 0u;
             const bool in = f < len && (key >> shift) == prefix;
-            const uint32_t bin = (key >> nshift) & ((1u << w) - 1u);
-            const uint32_t im = __ballot_sync(0xffffffffu, in);
-            if (!im) continue;
-            const int l0 = __ffs(im) - 1;
-            const uint32_t b0 = __shfl_sync(0xffffffffu, bin, l0);
-            if (__all_sync(0xffffffffu, !in || bin == b0)) {  // a warp of ties adds once
-                if (lane == l0) atomicAdd(&s_h2[b0], (uint32_t)__popc(im));
-            } else if (in) {
-                atomicAdd(&s_h2[bin], 1u);
-            }
+            hist_add_warp(s_h2, (key >> nshift) & ((1u << w) - 1u), in);
         }
         __syncthreads();
         select_bin<false>(s_h2, 1 << w, r, s_warp, s_sel);
@@ -632,29 +573,270 @@ __global__ void __launch_bounds__(kThreads, 1) prune_finish_kernel(PruneParams p
         above += s_sel[1];
         bincnt = s_sel[2];
         shift = nshift;
-        r = k - above;
+        r = target - above;
     }
-    // (above, tie) counts of every block before this CTA's range: keys above the
-    // first-digit bin from all keys, the rest from the candidates (or all keys)
+}
+
+struct StochArgs {
+    int64_t w;  // boundary pairs (0: deterministic top-k)
+    double prob;
+    unsigned long long seed;
+};
+
+__device__ __forceinline__ double swap_uniform(uint64_t seed, uint64_t i) {
+    uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// In-place descending bitonic sort of P (a power of two) 64-bit words in shared memory.
+__device__ __forceinline__ void bitonic_desc(unsigned long long *a, int P) {
+    for (int kk = 2; kk <= P; kk <<= 1)
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long x = a[i], y = a[ixj];
+                    if ((i & kk) == 0 ? x < y : x > y) {
+                        a[i] = y;
+                        a[ixj] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+}
+
+// Full passes over the N keys in shared memory use thread-contiguous chunks:
+// thread t owns keys [t c, (t+1) c) with c odd (at each step the 32 lanes of a
+// warp read 32 distinct banks), so thread order is flat order and a block scan of
+// per-thread counts gives every thread its flat-order start.
+__device__ __forceinline__ void my_chunk(int N, int &t0, int &t1) {
+    const int c = ((N + kThreads - 1) / kThreads) | 1;
+    t0 = min(N, (int)threadIdx.x * c);
+    t1 = min(N, t0 + c);
+}
+
+constexpr uint32_t kDirectRank = 64;  // bins up to this size: direct ranks (O(bc^2) compares; measured: at
+                                      // ~500 keys they cost 5 us, the two refinement digits ~1.5 us)
+
+// Exact threshold of the tgt-th largest key (tgt >= 1) from the first-digit
+// histogram in shared memory: keep keys (>> shift) > T and the first r keys
+// (>> shift) == T in flat order.  The boundary bin's keys are listed (key, flat
+// index; one pass, order free) and, when there are at most kDirectRank, each
+// computes its own rank among them directly -- rank = #(larger keys) + #(equal keys at
+// lower flat index) -- so the rank tgt-1 candidate gives the full key (shift 0)
+// and its tie quota.  Larger bins are refined digit by digit (refine_bin) over
+// the list, or over all keys when they exceed it.
+// PRE: also return this CTA's scan start `pre` = (above << 32 | tie) over the keys
+// at flat index < fpre, counted in the same passes (keys outside the boundary bin
+// during the list pass, the bin's own keys from the list).
+template <bool PRE>
+__device__ __forceinline__ void resolve_target(const uint32_t *s_key, int N, int t0, int t1, uint32_t tgt,
+                                               const uint32_t *s_h1, uint32_t *s_ck, uint32_t *s_cf,
+                                               uint32_t *s_h2, uint64_t *s_warp, uint32_t *s_sel,
+                                               uint32_t &T, int &shift, uint32_t &r, int fpre = 0,
+                                               uint64_t *pre = nullptr) {
+    select_bin<false>(s_h1, kH1, tgt, s_warp, s_sel);
+    uint32_t pf = s_sel[0], ab = s_sel[1], bc = s_sel[2];
+    shift = 19;
+    r = tgt - ab;
+    __syncthreads();
     uint32_t na = 0, nt = 0;
-    if (use_cand) {
-        for (int64_t f = threadIdx.x; f < f0; f += kThreads) na += (s_key[f] >> 19) > prefix1;
-        for (uint32_t i = threadIdx.x; i < nc; i += kThreads) {
-            if ((int64_t)s_cf[i] >= f0) continue;
-            const uint32_t kk = s_ck[i] >> shift;
-            na += kk > prefix;
-            nt += kk == prefix;
+    if (r >= bc || bc > (uint32_t)kSmallCand) {
+        if (r < bc)  // heavy ties: digit refinement over all keys
+            refine_bin(s_key, N, tgt, pf, shift, ab, bc, r, s_h2, s_warp, s_sel);
+        T = pf;      // else the whole bin is kept
+        if (PRE) {
+            for (int f = t0; f < min(t1, fpre); ++f) {
+                const uint32_t kk = s_key[f] >> shift;
+                na += kk > T;
+                nt += kk == T;
+            }
+            uint64_t tot;
+            block_excl_scan(((uint64_t)na << 32) | nt, s_warp, tot);
+            *pre = tot;
         }
-    } else {
-        for (int64_t f = threadIdx.x; f < f0; f += kThreads) {
-            const uint32_t kk = s_key[f] >> shift;
-            na += kk > prefix;
-            nt += kk == prefix;
+        return;
+    }
+    if (threadIdx.x == 0) s_sel[3] = 0;
+    __syncthreads();
+    for (int f = t0; f < t1; ++f) {
+        const uint32_t key = s_key[f];
+        const uint32_t d = key >> 19;
+        if (PRE) na += d > pf && f < fpre;
+        if (d == pf) {
+            const uint32_t pos = atomicAdd(&s_sel[3], 1u);
+            s_ck[pos] = key;
+            s_cf[pos] = (uint32_t)f;
         }
     }
-    uint64_t pre;
-    block_excl_scan(((uint64_t)na << 32) | nt, s_warp, pre);
-    scan_and_index(p, f0, f1, pre, prefix, shift, r, s_warp);
+    __syncthreads();
+    const uint32_t nc = bc;  // list length (refine_bin narrows bc)
+    if (bc > kDirectRank) {
+        refine_bin(s_ck, (int)bc, tgt, pf, shift, ab, bc, r, s_h2, s_warp, s_sel);
+        T = pf;
+    } else {
+        if (threadIdx.x < bc) {
+            const uint32_t ki = s_ck[threadIdx.x], fi = s_cf[threadIdx.x];
+            uint32_t gt = 0, eq = 0;
+            for (uint32_t j = 0; j < bc; ++j) {
+                const uint32_t kj = s_ck[j];
+                gt += kj > ki;
+                eq += kj == ki && s_cf[j] < fi;
+            }
+            if (gt + eq == r - 1) {  // exactly one candidate holds rank r-1 within the bin
+                s_sel[0] = ki;
+                s_sel[1] = r - gt;  // ties of ki kept: those at lower flat index and itself
+            }
+        }
+        __syncthreads();
+        T = s_sel[0];
+        r = s_sel[1];
+        shift = 0;
+    }
+    if (PRE) {
+        for (uint32_t i = threadIdx.x; i < nc; i += kThreads)
+            if ((int)s_cf[i] < fpre) {
+                const uint32_t kk = s_ck[i] >> shift;
+                na += kk > T;
+                nt += kk == T;
+            }
+        uint64_t tot;
+        block_excl_scan(((uint64_t)na << 32) | nt, s_warp, tot);
+        *pre = tot;
+    }
+    __syncthreads();
+}
+
+template <int ES, int B, bool STOCH>
+__global__ void __launch_bounds__(kThreads, 1) prune_finish_kernel(PruneParams p, StochArgs sa) {
+    extern __shared__ __align__(16) uint32_t s_dyn[];
+    __shared__ uint32_t s_h2[1024];
+    __shared__ uint64_t s_warp[32];
+    __shared__ uint32_t s_sel[4];
+    using G_ = Geo<ES, B>;
+    const int N = (int)p.N;
+    const int npad = (N + 3) & ~3;
+    uint32_t *s_key = s_dyn;                 // [npad] key bits, flat order (STOCH: then the final marks)
+    uint32_t *s_h1 = s_key + npad;           // [kH1] first-digit histogram
+    uint32_t *s_ck = s_h1 + kH1;             // [kSmallCand] candidate keys    | STOCH: [P] 64-bit boundary
+    uint32_t *s_cf = s_ck + kSmallCand;      // [kSmallCand] flat indices      |        list (sorted by rank)
+    for (int i = threadIdx.x; i < kH1; i += kThreads) s_h1[i] = 0;
+    pdl_wait();  // the sums kernel has completed: sumsq is final
+    // every key into shared memory (16-byte loads, 4 in flight per thread)
+    {
+        const float4 *src = reinterpret_cast<const float4 *>(p.sumsq);
+        const int n4 = N / 4;
+        for (int i0 = 0; i0 < n4; i0 += 4 * kThreads) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kThreads + threadIdx.x;
+                v[u] = i < n4 ? __ldcg(src + i) : float4{};
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kThreads + threadIdx.x;
+                if (i < n4)
+                    reinterpret_cast<uint4 *>(s_key)[i] =
+                        make_uint4(key_of(v[u].x), key_of(v[u].y), key_of(v[u].z), key_of(v[u].w));
+            }
+        }
+        for (int f = n4 * 4 + threadIdx.x; f < N; f += kThreads) s_key[f] = key_of(__ldcg(p.sumsq + f));
+    }
+    __syncthreads();
+    int t0, t1;
+    my_chunk(N, t0, t1);
+    for (int f = t0; f < t1; ++f) atomicAdd(&s_h1[s_key[f] >> 19], 1u);  // first digit (bits 30..19)
+    __syncthreads();
+    uint32_t pf, r;
+    int shift;
+    const int64_t u0 = (int64_t)blockIdx.x * p.units / gridDim.x;
+    const int64_t u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
+    auto flat_start = [&](int64_t u) -> int64_t {
+        return u >= p.units ? p.N : (u / p.upr) * p.nbc + (u % p.upr) * G_::G;
+    };
+    const int f0 = (int)flat_start(u0), f1 = (int)flat_start(u1);
+    uint64_t pre = 0;
+    if constexpr (!STOCH) {
+        resolve_target<true>(s_key, N, t0, t1, (uint32_t)p.k, s_h1, s_ck, s_cf, s_h2, s_warp, s_sel, pf, shift, r,
+                             f0, &pre);
+    } else {
+        // ranks [0, k - w) kept, [k - w, k + w) the boundary (R19)
+        const int w = (int)sa.w;
+        uint32_t T[2], rr[2];
+        int sh[2];
+        for (int t = 0; t < 2; ++t) {
+            const uint32_t tgt = (uint32_t)(t == 0 ? p.k - w : p.k + w);
+            if (tgt == 0) {  // empty selection: a prefix no key reaches
+                T[t] = 0xffffffffu;
+                sh[t] = 0;
+                rr[t] = 0;
+                continue;
+            }
+            resolve_target<false>(s_key, N, t0, t1, tgt, s_h1, s_ck, s_cf, s_h2, s_warp, s_sel, T[t], sh[t], rr[t]);
+        }
+        // marks in place of the keys: kept 0xffffffff, pruned 0x80000000, the 2w
+        // boundary blocks keep their key (< 2^31) until listed
+        constexpr uint32_t KEPT = 0xffffffffu, PRUNED = 0x80000000u;
+        uint32_t nA = 0, nB = 0;
+        for (int f = t0; f < t1; ++f) {
+            const uint32_t key = s_key[f];
+            nA += (key >> sh[0]) == T[0];
+            nB += (key >> sh[1]) == T[1];
+        }
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan(((uint64_t)nA << 32) | nB, s_warp, tot);
+        uint32_t bA = (uint32_t)(ex >> 32), bB = (uint32_t)ex, nbnd = 0;
+        for (int f = t0; f < t1; ++f) {
+            const uint32_t key = s_key[f];
+            const uint32_t kA = key >> sh[0], kB = key >> sh[1];
+            const bool inA = kA > T[0] || (kA == T[0] && bA < rr[0]);
+            const bool inB = kB > T[1] || (kB == T[1] && bB < rr[1]);
+            bA += kA == T[0];
+            bB += kB == T[1];
+            if (inA) s_key[f] = KEPT;
+            else if (inB) ++nbnd;
+            else s_key[f] = PRUNED;
+        }
+        uint32_t pb = (uint32_t)block_excl_scan(nbnd, s_warp, tot);
+        if ((uint32_t)tot != 2u * (uint32_t)w) __trap();  // |ranks [k - w, k + w)| = 2w by construction
+        unsigned long long *s_b = reinterpret_cast<unsigned long long *>(s_ck);
+        for (int f = t0; f < t1; ++f) {
+            const uint32_t v = s_key[f];
+            if (v < PRUNED) {
+                s_b[pb++] = ((unsigned long long)v << 32) | (0xffffffffu - (uint32_t)f);
+                s_key[f] = PRUNED;
+            }
+        }
+        int P = 1;
+        while (P < 2 * w) P <<= 1;
+        for (int i = 2 * w + threadIdx.x; i < P; i += kThreads) s_b[i] = 0ull;
+        __syncthreads();
+        bitonic_desc(s_b, P);
+        // sorted position j holds rank k - w + j: j < w stays kept unless pair w-1-j
+        // swaps, j >= w becomes kept iff pair j-w swaps
+        for (int j = threadIdx.x; j < 2 * w; j += kThreads) {
+            const int i = j < w ? w - 1 - j : j - w;
+            const bool swapped = swap_uniform(sa.seed, (uint64_t)i) < sa.prob;
+            if (j < w ? !swapped : swapped) s_key[0xffffffffu - (uint32_t)(s_b[j] & 0xffffffffull)] = KEPT;
+        }
+        __syncthreads();
+        pf = PRUNED;  // kept = mark > PRUNED, no ties taken
+        shift = 0;
+        r = 0;
+    }
+    if constexpr (STOCH) {  // kept blocks before this CTA's flat range (marks)
+        uint32_t na = 0;
+        for (int f = threadIdx.x; f < f0; f += kThreads) na += s_key[f] > pf;
+        uint64_t tot;
+        block_excl_scan((uint64_t)na << 32, s_warp, tot);
+        pre = tot;
+    }
+    scan_and_index(p, f0, f1, pre, pf, shift, r, s_warp, s_key);
     if (p.pdl_trig) pdl_trigger();
     pack_kept<ES, B>(p, u0, u1);
 }
@@ -943,6 +1125,37 @@ static int num_sms() {
     return sms;
 }
 
+// Dynamic shared memory of the small-N finishing kernel: keys, first-digit histogram, then the candidate list or (STOCH) the boundary list.
+static size_t small_smem_bytes(int64_t N, int64_t units, int64_t w) {
+    size_t tail = (size_t)kSmallCand * 8;
+    if (w > 0) {
+        int64_t P = 1;
+        while (P < 2 * w) P <<= 1;
+        tail = std::max(tail, (size_t)P * 8);
+    }
+    (void)units;
+    return (size_t)((N + 3) & ~int64_t(3)) * 4 + (size_t)kH1 * 4 + tail;
+}
+constexpr size_t kSmallSmemMax = 216 * 1024;  // + the kernel's static shared memory stays under 227 KB
+
+// The small-N pair: sums (no global histogram) -> finishing kernel, chained with PDL.
+template <int ES, int B, bool STOCH>
+static cudaError_t launch_small_t(PruneParams p, StochArgs sa, cudaStream_t stream) {
+    p.hist1 = nullptr;  // the finishing CTAs count the first digit themselves
+    const size_t smem = small_smem_bytes(p.N, p.units, STOCH ? sa.w : 0);
+    cudaError_t e = cudaFuncSetAttribute(prune_finish_kernel<ES, B, STOCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t per = kThreads / 32;  // one unit per warp
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((p.units + per - 1) / per, (int64_t)num_sms()));
+    e = launch_pdl(pdl_flags() & 128, prune_sums_kernel<ES, B>, dim3((unsigned)grid), dim3(kThreads), 0, stream, p);
+    if (e != cudaSuccess) return e;
+    count_launch();
+    e = launch_pdl(true, prune_finish_kernel<ES, B, STOCH>, dim3((unsigned)grid), dim3(kThreads), smem, stream, p, sa);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 template <int ES, int B>
 static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, const PruneWs &w) {
     if (p.k == 0) {
@@ -956,19 +1169,7 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
     }
     // (no per-launch memset: the kernels leave their workspace header zeroed, see above)
     cudaError_t e = cudaSuccess;
-    if (p.N <= kSmallN) {
-        const size_t smem = (size_t)((p.N + 3) & ~int64_t(3)) * 4 + (size_t)kSmallCand * 8;
-        e = cudaFuncSetAttribute(prune_finish_kernel<ES, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        const int64_t per = kThreads / 32;  // one unit per warp
-        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((p.units + per - 1) / per, (int64_t)num_sms()));
-        e = launch_pdl(pdl_flags() & 128, prune_sums_kernel<ES, B>, dim3((unsigned)grid), dim3(kThreads), 0, stream, p);
-        if (e != cudaSuccess) return e;
-        count_launch();
-        e = launch_pdl(true, prune_finish_kernel<ES, B>, dim3((unsigned)grid), dim3(kThreads), smem, stream, p);
-        count_launch();
-        return e != cudaSuccess ? e : cudaGetLastError();
-    }
+    if (p.N <= kSmallN) return launch_small_t<ES, B, false>(p, StochArgs{0, 0.0, 0ull}, stream);
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, prune_kernel<ES, B>, kThreads, 0);
     if (e != cudaSuccess) return e;
@@ -1153,14 +1354,6 @@ StochWs stoch_ws_layout(int64_t N) {
     return w;
 }
 
-__device__ __forceinline__ double swap_uniform(uint64_t seed, uint64_t i) {
-    uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    z ^= z >> 31;
-    return (double)(z >> 11) * (1.0 / 9007199254740992.0);
-}
-
 // One CTA: resolve the next key digit of both selections (targets A, B) from the
 // histogram, then zero the histogram (self-cleaning workspace).
 __global__ void __launch_bounds__(kThreads) stoch_update_kernel(int level, uint32_t *hist, uint32_t *st,
@@ -1339,21 +1532,7 @@ __global__ void __launch_bounds__(1024) stoch_swap_kernel(unsigned long long *__
     for (int i = threadIdx.x; i < P; i += blockDim.x) s_b[i] = i < n ? __ldcg(blist + i) : 0ull;
     __syncthreads();
     if (threadIdx.x == 0) *bcount = 0;
-    for (int kk = 2; kk <= P; kk <<= 1)
-        for (int j = kk >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < P; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const unsigned long long a = s_b[i], b2 = s_b[ixj];
-                    const bool desc = (i & kk) == 0;
-                    if (desc ? a < b2 : a > b2) {
-                        s_b[i] = b2;
-                        s_b[ixj] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
+    bitonic_desc(s_b, P);
     // sorted position j holds rank A + j: j < w is kept unless pair w-1-j swaps,
     // j >= w is kept iff pair j-w swaps
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
@@ -1426,6 +1605,10 @@ __global__ void __launch_bounds__(kThreads, (B >= 16) ? 1 : 2) stoch_pack_kernel
 template <int ES, int B>
 static cudaError_t launch_stoch_t(PruneParams p, StochParams q, int64_t wn, double prob,
                                   uint64_t seed, cudaStream_t stream) {
+    // the two-kernel path while every CTA can hold all keys and the boundary list
+    // (N up to ~43K keys: S12 fc2 at b = 16 included); the multi-kernel path beyond
+    if (small_smem_bytes(p.N, p.units, wn) <= kSmallSmemMax)
+        return launch_small_t<ES, B, true>(p, StochArgs{wn, prob, (unsigned long long)seed}, stream);
     const int sms = num_sms();
     const int64_t per = kThreads / 32;
     const int64_t sgrid = std::max<int64_t>(1, std::min<int64_t>((p.units + per - 1) / per, (int64_t)sms));

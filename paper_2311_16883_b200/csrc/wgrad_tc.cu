@@ -1095,21 +1095,7 @@ static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms) {
     int64_t ns = std::max<int64_t>(1, cap / std::max<int64_t>(1, tiles));
     if (C::X3) {  // chain cap: at most kX3ChainRows rows of MMAs per TMEM accumulator
         const int64_t steps_cap = std::max<int64_t>(1, kX3ChainRows / C::SROWS);
-        const int64_t ns_min = std::max<int64_t>(ns, (nst + steps_cap - 1) / steps_cap);
-        // Beyond one wave of CTAs (one per SM), pick the split count in [ns_min, 2 ns_min]
-        // that minimises waves x steps per split: ns_min itself can leave the last wave
-        // mostly empty (C2: 17 splits = 408 CTAs = 2.76 waves of 47 steps; 18 = 2.92 of 44).
-        ns = ns_min;
-        if (tiles * ns_min > cap) {
-            int64_t best = -1;
-            for (int64_t c = ns_min; c <= 2 * ns_min; ++c) {
-                const int64_t cost = ((tiles * c + cap - 1) / cap) * ((nst + c - 1) / c);
-                if (best < 0 || cost < best) {
-                    best = cost;
-                    ns = c;
-                }
-            }
-        }
+        ns = std::max<int64_t>(ns, (nst + steps_cap - 1) / steps_cap);
     }
     pl.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>({nst, ns, (int64_t)kMaxSplits}));
     return pl;

@@ -135,3 +135,14 @@ def test_stochastic_workspace_reuse_across_shapes():
     for nbr in (30, 9, 50):
         X = synth.ints(nbr * 4, 16 * 4, seed=nbr, lo=-20, hi=20)
         compare(X, 4, nbr * 8, 100, 0.7, seed=nbr)
+
+
+def test_stochastic_small_n_limit_b64():
+    """N = kSmallN = 24576 keys at b = 64 with the largest window: the largest
+    shared-memory footprint of the one-kernel finishing path (all keys + the
+    8192-entry boundary list per CTA)."""
+    b, nbr, nbc = 64, 96, 256
+    X = synth.ints(nbr * b, nbc * b, seed=12, lo=-3, hi=3)
+    h = synth.to_bf16_bits(X)
+    compare(h, b, 12288, 4096, 0.5, seed=4, bf16=True)
+    compare(h, b, 12288, 1000, 0.5, seed=4, bf16=True)

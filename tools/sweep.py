@@ -284,9 +284,35 @@ def sweep_fusion(out, hbm, reps=20, nsets=3):
     return rows
 
 
+def sweep_stoch(out, hbm, reps=20, nsets=4):
+    """f4 stochastic boundary swapping (R19) vs the deterministic prune on the S12
+    layers at batch 128: device time and algorithmic GB/s of each (same bytes:
+    X read once, k blocks written)."""
+    rows = []
+    for lname, M, K, fam in (("fc1", 25088, 384, "aff"), ("fc2", 25088, 1536, "gelu")):
+        Xs = [activation(M, K, fam, SEED + 40 * i + 3, torch.float32) for i in range(nsets)]
+        for b in (16, 32):
+            keep = 0.5
+            N = bp.num_blocks(M, K, b)
+            k = bp.keep_count(N, keep)
+            alg = metrics.prune_bytes(M, K, b, k, 4)
+            outs = [bp.prune(X, b, k=k) for X in Xs]
+            t_p = timed(lambda j: bp.prune(Xs[j], b, k=k, out=outs[j]), Xs, reps)
+            for window in (64, 1024, 4096):
+                t_s = timed(lambda j: bp.prune_stochastic(Xs[j], b, k=k, window=window, p=0.5, seed=j, out=outs[j]),
+                            Xs, reps)
+                row = dict(config="f4-stochastic", layer=lname, M=M, K=K, b=b, keep=keep, N=N, k=k, window=window,
+                           p=0.5, prune_ms=t_p, stoch_ms=t_s, prune_hbm_frac=alg / (t_p * 1e-3) / 1e9 / hbm,
+                           stoch_hbm_frac=alg / (t_s * 1e-3) / 1e9 / hbm)
+                rows.append(row)
+                print(json.dumps(row), flush=True)
+                out.write(json.dumps(row) + "\n")
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", nargs="+", choices=["c3", "c5", "global", "rows", "fusion"])
+    ap.add_argument("which", nargs="+", choices=["c3", "c5", "global", "rows", "fusion", "stoch"])
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out", "sweep"))
     a = ap.parse_args()
     os.makedirs(a.out_dir, exist_ok=True)
@@ -304,6 +330,8 @@ def main():
                 sweep_global(out, hbm)
             elif w == "rows":
                 sweep_rows(out, hbm)
+            elif w == "stoch":
+                sweep_stoch(out, hbm)
             else:
                 sweep_fusion(out, hbm)
 
