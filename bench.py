@@ -12,6 +12,9 @@ FP32-grade dW (3xTF32 tensor cores, rel-F <= 1e-5); the tf32 / bf16 dW of the
 same layer are reported as extra keys.  At N > 1 every rank runs its own such
 shard (weak scaling) and the partial dW are all-reduced.
 
+--config C3: BASELINE.json configs[2], ResMLP-S12's 12 x (fc1, fc2) layers at batch
+128 (same step structure as C4 below), fp32 activations / FP32-grade dW by default.
+
 --config C4: BASELINE.json configs[3], ResMLP-B24 (dim 768, hidden 3072) at a
 total batch of 1024 x 196 tokens sharded over the N ranks (strong scaling): one
 step = prune + decompress of the inputs of all 24 x (fc1, fc2) layers, then
@@ -24,6 +27,7 @@ max-over-ranks device time of the K timed steps, in GB/s; per-kernel GB/s,
 TFLOP/s and roofline fractions are in `kernels` / `roofline`.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--dtype f32|bf16]
+    python bench.py --config C3                          # S12, all 24 linear layers
     python bench.py --config C4 --gpus 8                # B24 strong scaling
     python bench.py --impl reference ...   # the CPU oracle arm
 
@@ -63,7 +67,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
-    ap.add_argument("--config", default="C2", choices=sorted(synth.CONFIGS) + ["C4"])
+    ap.add_argument("--config", default="C2", choices=sorted(synth.CONFIGS) + ["C3", "C4"])
     ap.add_argument("--dtype", choices=["f32", "bf16"], default=None,
                     help="element type of X and dY (default f32; bf16 for --config C4)")
     ap.add_argument("--prec", choices=["fp32", "tf32", "bf16"], default=None,
@@ -104,7 +108,8 @@ def maybe_spawn(a) -> int | None:
 
 
 def workload(a):
-    c = dict(synth.CONFIGS["C4_fc1" if a.config == "C4" else a.config])
+    # model steps (C3, C4): their per-layer oracle / cpu legs use the first layer's shape
+    c = dict(synth.CONFIGS[{"C3": "C2", "C4": "C4_fc1"}.get(a.config, a.config)])
     if a.b is not None:
         c["b"] = a.b
     if a.keep is not None:
@@ -392,8 +397,8 @@ def run_native(a):
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if a.config == "C4":
-        return run_c4(a, rank, local, world, dev)
+    if a.config in MODELS:
+        return run_model(a, rank, local, world, dev)
     c = workload(a)
     M, K, N, b, keep = c["M"], c["K"], c["N"], c["b"], c["keep"]
     tdt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
@@ -679,44 +684,56 @@ def run_native(a):
     return 0
 
 
-# ----------------------------------------------------------------------------- C4: ResMLP-B24, strong scaling
-B24_BLOCKS, B24_DIM, B24_HIDDEN, B24_ROWS = 24, 768, 3072, 1024 * 196
+# ----------------------------------------------------------------------------- model steps (C3, C4)
+# Whole-model steps over every linear layer of a ResMLP: BASELINE.json configs[2]
+# (C3: S12, 12 blocks, dim 384, hidden 1536, batch 128) and configs[3] (C4: B24,
+# 24 blocks, dim 768, hidden 3072, batch 1024), the batch rows sharded over the
+# ranks (strong scaling).
+MODELS = {
+    "C3": dict(name="ResMLP-S12", blocks=12, dim=384, hidden=1536, rows=128 * 196, cfg_id=3,
+               what="C3: ResMLP-S12 (dim 384, hidden 1536), all 12 x (fc1, fc2) linear layers, batch 128 x 196 "
+                    "tokens sharded over the ranks"),
+    "C4": dict(name="ResMLP-B24", blocks=24, dim=768, hidden=3072, rows=1024 * 196, cfg_id=4,
+               what="C4: ResMLP-B24 (dim 768, hidden 3072), 24 x (fc1, fc2), total batch 1024 x 196 "
+                    "tokens sharded over the ranks"),
+}
 
 
-def run_c4(a, rank, local, world, dev):
-    """BASELINE configs[3]: ResMLP-B24 at total batch 1024 (200704 rows) sharded
-    over the ranks (strong scaling).  One step on a rank: for each of the 24 x 2
-    linear layers (fc1: 768 -> 3072, fc2: 3072 -> 768) prune + decompress its
-    input shard; then the dW of every layer in backward order, each written into
-    an all-reduce bucket that goes out on the communication stream as soon as it
-    is complete (a7 overlapped with the remaining dW)."""
+def run_model(a, rank, local, world, dev):
+    """One step on a rank: for each of the blocks x 2 linear layers (fc1: dim ->
+    hidden, fc2: hidden -> dim) prune + decompress its input shard; then the dW of
+    every layer in backward order, each written into an all-reduce bucket that goes
+    out on the communication stream as soon as it is complete (a7 overlapped with
+    the remaining dW)."""
     import torch
 
     import paper_2311_16883_b200 as bp
     from paper_2311_16883_b200 import dist as D
 
+    mdl = MODELS[a.config]
     b = a.b or 32
     keep = 0.5 if a.keep is None else a.keep
-    r0, r1 = D.shard_rows(B24_ROWS, world, rank, 196 * b // math.gcd(196, b))
+    r0, r1 = D.shard_rows(mdl["rows"], world, rank, 196 * b // math.gcd(196, b))
     M = r1 - r0
     tdt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
     s_x = 2 if a.dtype == "bf16" else 4
     lib = bp._lib.load()
-    shapes = [(B24_DIM, B24_HIDDEN), (B24_HIDDEN, B24_DIM)]  # (K, N) of fc1, fc2
+    shapes = [(mdl["dim"], mdl["hidden"]), (mdl["hidden"], mdl["dim"])]  # (K, N) of fc1, fc2
     # rotating activation / gradient sets: consecutive layers never share inputs, and every
-    # set (>= 77 MB at 8 ranks) is separated from its next use by > 2x L2 of other traffic
-    NS = 4 if M <= 50176 else 2
+    # set is separated from its next use by > 2x L2 of other traffic
+    set_bytes = M * (shapes[0][0] + shapes[0][1]) * s_x
+    NS = max(2, min(4, math.ceil(4 * L2_BYTES / max(1, 2 * set_bytes))))
     X = {t: [] for t in range(2)}
     dY = {t: [] for t in range(2)}
     for t, (K, N) in enumerate(shapes):
         fam = "aff" if t == 0 else "gelu"
         for j in range(NS):
-            seed = synth.seed_for(4, 10 * t + j, rank)
+            seed = synth.seed_for(mdl["cfg_id"], 10 * t + j, rank)
             X[t].append(to_dev(synth.to_bf16_bits(synth.activation(fam, M, K, seed)) if a.dtype == "bf16"
                                else synth.activation(fam, M, K, seed), a.dtype, dev))
             g = synth.grad_out(M, N, seed)
             dY[t].append(to_dev(synth.to_bf16_bits(g) if a.dtype == "bf16" else g, a.dtype, dev))
-    layers = [(l, t) for l in range(B24_BLOCKS) for t in range(2)]  # forward order
+    layers = [(l, t) for l in range(mdl["blocks"]) for t in range(2)]  # forward order
     ks = {t: bp.keep_count(bp.num_blocks(M, shapes[t][0], b), keep) for t in range(2)}
     bsrs = {lt: bp.alloc_bsr(M, shapes[lt[1]][0], b, ks[lt[1]], tdt, dev) for lt in layers}
     Xd = {t: torch.empty(M, shapes[t][0], dtype=tdt, device=dev) for t in range(2)}
@@ -791,11 +808,11 @@ def run_c4(a, rank, local, world, dev):
         "metric": METRIC, "value": bytes_all / (t_ms_max * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": per_rank_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": f"{a.dtype} (dW {a.prec})", "data": "synthetic",
-        "config": {"workload": "C4: ResMLP-B24 (dim 768, hidden 3072), 24 x (fc1, fc2), total batch 1024 x 196 "
-                               "tokens sharded over the ranks", "rows_per_rank": M, "b": b, "keep": keep,
-                   "x_dtype": a.dtype, "dw_prec": a.prec, "global_batch_rows": B24_ROWS,
+        "config": {"workload": mdl["what"], "rows_per_rank": M, "b": b, "keep": keep,
+                   "x_dtype": a.dtype, "dw_prec": a.prec, "global_batch_rows": mdl["rows"],
                    "parallelism": f"dp{world}", "bucket_mb": a.bucket_mb, "buckets": len(bucket.buckets),
-                   "l2": f"{NS} rotating activation sets (>= 77 MB each at 8 ranks; consecutive layers differ)"},
+                   "l2": f"{NS} rotating activation/gradient sets of {set_bytes / 1e6:.0f} MB per layer type "
+                         "(consecutive layers differ)"},
         "wgrad_tflops": flops_all / (t_ms_max * 1e-3) / 1e12,
         "wgrad_tc_frac_of_step": flops_all / (t_ms_max * 1e-3) / 1e12 / (peak * world),
         "phases_ms": ph,

@@ -234,6 +234,22 @@ BSR_API bsr_status_t bsr_wgrad_algo(const bsr_t *A, const void *dY, int32_t dy_d
                                     int32_t accumulate, int32_t prec, int32_t algo, void *ws, size_t ws_bytes,
                                     void *stream);
 
+/* BSR_DW_NK: the same weight gradient stored transposed, dWt = dW^T (N x K
+ * row-major fp32 -- PyTorch's nn.Linear.weight.grad layout, so a layer's backward
+ * needs no transpose):  dWt[n][J*b + c] (+)= sum ... (as bsr_wgrad_algo).
+ * Same prec / algo / operand rules as bsr_wgrad_algo.  The FP32-grade per-run
+ * kernel (b in {32, 64}, N % 128 == 0) writes it natively: its chain-capped
+ * split-K reduce sums the partials in split order (bit-identical to bsr_wgrad's
+ * dW, transposed) and stores through a 32 x 32 shared-memory transpose; every
+ * other path computes dW into the workspace's tail and transposes it in one
+ * extra pass (accumulate then adds old + dW, one rounding).  ws: at least
+ * bsr_wgrad_nk_workspace_bytes(M, K, b, N, prec, algo) bytes, 16-byte aligned,
+ * not overlapping dWt. */
+BSR_API size_t bsr_wgrad_nk_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec, int32_t algo);
+BSR_API bsr_status_t bsr_wgrad_nk(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dWt,
+                                  int32_t accumulate, int32_t prec, int32_t algo, void *ws, size_t ws_bytes,
+                                  void *stream);
+
 /* dW with the data-parallel sum fused into it (a7 over NVLink
  * SHARP): mc_dW is the MULTIMEM (NVLS multicast) address of a K x N fp32 buffer
  * bound on every rank (e.g. torch symmetric memory's multicast_ptr); this rank's

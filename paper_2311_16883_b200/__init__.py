@@ -251,28 +251,35 @@ def decompress(A: BSR, out: torch.Tensor | None = None, stream=None) -> torch.Te
 
 
 def wgrad(A: BSR, dY: torch.Tensor, prec: str = "fp32", out: torch.Tensor | None = None,
-          accumulate: bool = False, stream=None, algo: str = "auto") -> torch.Tensor:
+          accumulate: bool = False, stream=None, algo: str = "auto", layout: str = "kn") -> torch.Tensor:
     """dW = X_bsr^T . dY (K x N fp32) over the kept blocks only.
 
     prec: "fp32" (FP32 grade, rel-F <= 1e-5: 3xTF32 tensor cores or FFMA), "tf32"
     or "bf16" (tensor cores, <= 5e-3).  algo: "auto" (the library's per-shape
-    choice), "runs", "span" (the two tcgen05 kernels) or "simt" (FFMA)."""
+    choice), "runs", "span" (the two tcgen05 kernels) or "simt" (FFMA).
+    layout: "kn" (K x N) or "nk" (dW^T, N x K: nn.Linear.weight.grad's layout,
+    bsr_wgrad_nk)."""
     lib = _lib.load()
     dY = _cuda2d(dY, "dY")
     if dY.shape[0] != A.M:
         raise ValueError(f"dY has {dY.shape[0]} rows, BSR has M={A.M}")
+    if layout not in ("kn", "nk"):
+        raise ValueError(f"layout must be 'kn' or 'nk', got {layout!r}")
     N = dY.shape[1]
+    shape = (A.K, N) if layout == "kn" else (N, A.K)
     if out is None:
-        out = torch.empty((A.K, N), dtype=torch.float32, device=dY.device)
+        out = torch.empty(shape, dtype=torch.float32, device=dY.device)
     else:
-        _check_dense_out(out, (A.K, N), torch.float32, dY.device, "out")
+        _check_dense_out(out, shape, torch.float32, dY.device, "out")
     p = PREC[prec]
-    ws_bytes = lib.bsr_wgrad_algo_workspace_bytes(A.M, A.K, A.b, N, p, ALGO[algo])
+    if layout == "kn":
+        fn, ws_bytes = lib.bsr_wgrad_algo, lib.bsr_wgrad_algo_workspace_bytes(A.M, A.K, A.b, N, p, ALGO[algo])
+    else:
+        fn, ws_bytes = lib.bsr_wgrad_nk, lib.bsr_wgrad_nk_workspace_bytes(A.M, A.K, A.b, N, p, ALGO[algo])
     ws = workspace(ws_bytes, dY.device, stream=stream) if ws_bytes else None
     cs = A.c_struct()
-    _lib.check(lib.bsr_wgrad_algo(ctypes.byref(cs), dY.data_ptr(), _dt(dY), N, out.data_ptr(), int(accumulate), p,
-                                  ALGO[algo], ws.data_ptr() if ws is not None else None,
-                                  ws.numel() if ws is not None else 0, _stream(stream)))
+    _lib.check(fn(ctypes.byref(cs), dY.data_ptr(), _dt(dY), N, out.data_ptr(), int(accumulate), p, ALGO[algo],
+                  ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0, _stream(stream)))
     return out
 
 

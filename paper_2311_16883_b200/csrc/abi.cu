@@ -636,6 +636,45 @@ bsr_status_t bsr_wgrad_algo(const bsr_t *A, const void *dY, int32_t dy_dtype, in
                        "bsr_wgrad (tensor-core) launch");
 }
 
+size_t bsr_wgrad_nk_workspace_bytes(int64_t M, int64_t K, int32_t b, int64_t N, int32_t prec, int32_t algo) {
+    if (bsr_num_blocks(M, K, b) < 0 || N <= 0) return 0;
+    return align256(bsr_wgrad_algo_workspace_bytes(M, K, b, N, prec, algo)) + align256((size_t)K * N * sizeof(float));
+}
+
+bsr_status_t bsr_wgrad_nk(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dWt, int32_t accumulate,
+                          int32_t prec, int32_t algo, void *ws, size_t ws_bytes, void *stream) {
+    bsr_status_t st = check_bsr(A);
+    if (st != BSR_OK) return st;
+    if (N <= 0 || N > (int64_t(1) << 30)) return fail(BSR_ERR_SHAPE, "N=%lld out of range", (long long)N);
+    if (!dY || !dWt) return fail(BSR_ERR_INVALID_ARG, "dY or dWt is NULL");
+    if (accumulate != 0 && accumulate != 1) return fail(BSR_ERR_INVALID_ARG, "accumulate must be 0 or 1");
+    if (!aligned16(dWt)) return fail(BSR_ERR_ALIGNMENT, "dWt is not 16-byte aligned");
+    const int esy = elem_size(dy_dtype);
+    if (esy == 0) return fail(BSR_ERR_INVALID_ARG, "dy_dtype %d is not BSR_DT_F32 or BSR_DT_BF16", dy_dtype);
+    const size_t dw_bytes = (size_t)A->K * N * 4;
+    if (overlap(dWt, dw_bytes, dY, (size_t)A->M * N * esy)) return fail(BSR_ERR_INVALID_ARG, "dWt overlaps dY");
+    const size_t inner = bsr_wgrad_algo_workspace_bytes(A->M, A->K, A->b, N, prec, algo);
+    const size_t need = align256(inner) + align256(dw_bytes);
+    st = check_wgrad_ws(need, ws, ws_bytes, dWt, dw_bytes);
+    if (st != BSR_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // native: the FP32-grade per-run kernel's chain-capped split-K reduce stores dW^T directly
+    const bool dense_auto = algo == BSR_ALGO_AUTO && A->b < 32;
+    if (prec == BSR_PREC_FP32 && !dense_auto && (algo == BSR_ALGO_AUTO || algo == BSR_ALGO_TC_RUNS) &&
+        A->dtype == BSR_DT_F32 && dy_dtype == BSR_DT_F32 && A->nnzb > 0 && aligned16(dY) && (N * 4) % 16 == 0 &&
+        bsrp::wgrad_tc_supported(2, BSR_ALGO_TC_RUNS, A->b, A->K, N) && bsrp::wgrad_x3_native_nk(A->M, A->K, A->b, N)) {
+        cudaError_t e = bsrp::launch_wgrad_tc(A->rowptr, A->colidx, A->values, A->nnzb, 2, BSR_ALGO_TC_RUNS, A->M,
+                                              A->K, A->b, dY, N, dWt, accumulate, ws, s, nullptr, 1);
+        if (e != cudaErrorNotSupported) return cuda_status(e, "bsr_wgrad_nk (fp32 grade, 3xTF32) launch");
+        (void)cudaGetLastError();
+    }
+    // any other path: dW (K x N) into the workspace's tail, then one transposing pass
+    float *scratch = reinterpret_cast<float *>(static_cast<char *>(ws) + align256(inner));
+    st = bsr_wgrad_algo(A, dY, dy_dtype, N, scratch, 0, prec, algo, inner ? ws : nullptr, inner, stream);
+    if (st != BSR_OK) return st;
+    return cuda_status(bsrp::launch_transpose_reduce(scratch, dWt, A->K, N, 1, accumulate, s), "bsr_wgrad_nk transpose");
+}
+
 bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *dW, int32_t accumulate,
                        int32_t prec, void *ws, size_t ws_bytes, void *stream) {
     return bsr_wgrad_algo(A, dY, dy_dtype, N, dW, accumulate, prec, BSR_ALGO_AUTO, ws, ws_bytes, stream);

@@ -591,34 +591,19 @@ __device__ __forceinline__ double swap_uniform(uint64_t seed, uint64_t i) {
     return (double)(z >> 11) * (1.0 / 9007199254740992.0);
 }
 
-// In-place descending bitonic sort of P (a power of two) 64-bit words in shared
-// memory.  Each pass visits the P/2 compare-exchange pairs (i, i | j) directly --
-// pair q -> i = q with a 0 bit inserted at log2(j) -- with up to 8 pairs per
-// thread loaded before any is compared, so a pass costs one round of shared-memory
-// latency instead of one per element (the sort is latency-bound: 91 passes at P = 8192).
+// In-place descending bitonic sort of P (a power of two) 64-bit words in shared memory.
+// (A variant visiting the P/2 pairs directly with 8 loads in flight per thread
+// was no faster in the stochastic sweep -- profiles/r02e vs r02d -- and was dropped.)
 __device__ __forceinline__ void bitonic_desc(unsigned long long *a, int P) {
-    const int T = blockDim.x, npairs = P >> 1;
     for (int kk = 2; kk <= P; kk <<= 1)
         for (int j = kk >> 1; j > 0; j >>= 1) {
-            const int lj = __ffs(j) - 1;
-            for (int q0 = threadIdx.x; q0 < npairs; q0 += 8 * T) {
-                unsigned long long x[8], y[8];
-                int ii[8];
-#pragma unroll
-                for (int m = 0; m < 8; ++m) {
-                    const int q = q0 + m * T;
-                    ii[m] = ((q >> lj) << (lj + 1)) | (q & (j - 1));
-                    if (q < npairs) {
-                        x[m] = a[ii[m]];
-                        y[m] = a[ii[m] | j];
-                    }
-                }
-#pragma unroll
-                for (int m = 0; m < 8; ++m) {
-                    if (q0 + m * T >= npairs) continue;
-                    if ((ii[m] & kk) == 0 ? x[m] < y[m] : x[m] > y[m]) {
-                        a[ii[m]] = y[m];
-                        a[ii[m] | j] = x[m];
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long x = a[i], y = a[ixj];
+                    if ((i & kk) == 0 ? x < y : x > y) {
+                        a[i] = y;
+                        a[ixj] = x;
                     }
                 }
             }

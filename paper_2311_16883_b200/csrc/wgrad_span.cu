@@ -676,6 +676,13 @@ static cudaError_t make_map(CUtensorMap *tm, const void *base, CUtensorMapDataTy
     auto fn = encode_fn();
     if (!fn) return cudaErrorNotSupported;
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    // The encoder is a driver-API call: it needs the device's context current in
+    // this thread, which the runtime only makes current lazily.  A thread whose
+    // first CUDA work is this call (e.g. PyTorch's autograd worker reusing cached
+    // allocations) would get CUDA_ERROR_INVALID_CONTEXT; cudaSetDevice makes the
+    // primary context current.
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaSetDevice(dev) != cudaSuccess) return cudaErrorInvalidDevice;
     CUresult r = fn(tm, dt, rank, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;

@@ -39,6 +39,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 
@@ -1047,6 +1048,13 @@ static cudaError_t make_map(CUtensorMap *tm, const void *base, CUtensorMapDataTy
     auto fn = encode_fn();
     if (!fn) return cudaErrorNotSupported;
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    // The encoder is a driver-API call: it needs the device's context current in
+    // this thread, which the runtime only makes current lazily.  A thread whose
+    // first CUDA work is this call (e.g. PyTorch's autograd worker reusing cached
+    // allocations) would get CUDA_ERROR_INVALID_CONTEXT; cudaSetDevice makes the
+    // primary context current.
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaSetDevice(dev) != cudaSuccess) return cudaErrorInvalidDevice;
     CUresult r = fn(tm, dt, rank, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     swz(swizzle_bytes), CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
@@ -1104,13 +1112,14 @@ static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms) {
 template <int KIND, int B>
 static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
                             int64_t M, int64_t K, const void *dY, int64_t N, float *dW, int accumulate,
-                            float *ws, cudaStream_t stream, float *mc) {
+                            float *ws, cudaStream_t stream, float *mc, int nk) {
     using C = Cfg<KIND, B>;
     int dev = 0, sms = kSplitSMs;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const Plan pl = plan_for<KIND, B>(M, K, N, sms);
     if (pl.chunk_steps < 1) return cudaErrorNotSupported;  // K / b too large for the chunk buffers
+    if (nk && (pl.nsplit < 2 || mc)) return cudaErrorNotSupported;  // dW^T only through the split-K reduce
     const CUtensorMapDataType dt = KIND == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     // dY (N x M, row-major): one box = the SROWS x 128 slab of a step, row-major
     // in shared memory (no swizzle: the A movers read it column-wise)
@@ -1170,6 +1179,7 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess || pl.nsplit == 1) return e;
+    if (nk) return launch_transpose_reduce(ws, dW, K, N, pl.nsplit, accumulate, stream);
     const int64_t n4 = K * N / 4;
     const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 4));
     e = launch_pdl(pdl_flags() & 32, splitk_reduce_kernel, dim3(rgrid), dim3(256), 0, stream, reinterpret_cast<const float4 *>(ws),
@@ -1177,6 +1187,38 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
                    reinterpret_cast<float4 *>(mc));
     count_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// dW^T (N x K, row-major: PyTorch's Linear.weight.grad layout; BSR_DW_NK) (+)=
+// the sum over splits of K x N partial tiles, in split order -- the same adds as
+// splitk_reduce_kernel, stored transposed through a 32 x 32 shared-memory tile
+// (reads coalesced along N, writes along K).
+__global__ void __launch_bounds__(256) transpose_reduce_kernel(const float *__restrict__ ws, float *__restrict__ dWt,
+                                                               int64_t K, int64_t N, int nsplit, int accumulate) {
+    __shared__ float tile[32][33];
+    pdl_wait();
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+    const int64_t ntn = (N + 31) / 32, ntiles = ntn * ((K + 31) / 32);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t k0 = (t / ntn) * 32, n0 = (t % ntn) * 32;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int64_t k = k0 + ty + 8 * r, n = n0 + tx;
+            float a = 0.f;
+            if (k < K && n < N) {
+                if (accumulate) a = dWt[n * K + k];
+                for (int s = 0; s < nsplit; ++s) a += __ldcs(ws + ((int64_t)s * K + k) * N + n);
+            }
+            tile[ty + 8 * r][tx] = a;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int64_t n = n0 + ty + 8 * r, k = k0 + tx;
+            if (k < K && n < N) dWt[n * K + k] = tile[tx][ty + 8 * r];
+        }
+        __syncthreads();
+    }
 }
 
 }  // namespace tc
@@ -1192,6 +1234,29 @@ cudaError_t launch_splitk_reduce(const float *ws, float *dW, int64_t n, int nspl
                                accumulate, (pdl_flags() & 8) ? 1 : 0, static_cast<float4 *>(nullptr));
     count_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_transpose_reduce(const float *ws, float *dWt, int64_t K, int64_t N, int nsplit, int accumulate,
+                                    cudaStream_t stream) {
+    int dev = 0, sms = tc::kSplitSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = ((N + 31) / 32) * ((K + 31) / 32);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * 8));
+    cudaError_t e = launch_pdl(pdl_flags() & 32, tc::transpose_reduce_kernel, dim3(grid), dim3(256), 0, stream, ws, dWt, K,
+                               N, nsplit, accumulate);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// FP32 grade per-run plan with more than one split: its split-K reduce can store
+// dW^T directly (bsr_wgrad_nk's native path).
+bool wgrad_x3_native_nk(int64_t M, int64_t K, int b, int64_t N) {
+    tc::Plan pl{};
+    if (b == 32) pl = tc::plan_for<2, 32>(M, K, N, tc::kSplitSMs);
+    else if (b == 64) pl = tc::plan_for<2, 64>(M, K, N, tc::kSplitSMs);
+    else return false;
+    return pl.nsplit > 1 && pl.chunk_steps >= 1;
 }
 
 static size_t wgrad_runs_ws_bytes(int64_t M, int64_t K, int b, int64_t N) {
@@ -1251,16 +1316,17 @@ bool wgrad_tc_supported(int kind, int algo, int b, int64_t K, int64_t N) {
 
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
                             int kind, int algo, int64_t M, int64_t K, int b, const void *dY, int64_t N, float *dW,
-                            int accumulate, void *ws, cudaStream_t stream, float *mc) {
-    if (mc && !use_runs_kernel(kind, algo, b, K)) return cudaErrorNotSupported;  // multicast: per-run kernel only
+                            int accumulate, void *ws, cudaStream_t stream, float *mc, int nk) {
+    if ((mc || nk) && !use_runs_kernel(kind, algo, b, K)) return cudaErrorNotSupported;  // per-run kernel only
     if (!use_runs_kernel(kind, algo, b, K))
         return launch_wgrad_span(rowptr, colidx, values, nnzb, kind, M, K, b, dY, N, dW, accumulate, ws, stream);
     if (!values || nnzb == 0) {  // no stored block: dW = 0 (or unchanged; nothing to add into the multicast dW)
+        if (nk) return cudaErrorNotSupported;
         return accumulate || mc ? cudaSuccess : cudaMemsetAsync(dW, 0, (size_t)K * N * sizeof(float), stream);
     }
 #define TC_CASE(KD, B_) \
     if (kind == KD && b == B_) return tc::launch_t<KD, B_>(rowptr, colidx, values, nnzb, M, K, dY, N, dW, accumulate, \
-                                                            static_cast<float *>(ws), stream, mc);
+                                                            static_cast<float *>(ws), stream, mc, nk);
     TC_CASE(0, 32) TC_CASE(0, 64) TC_CASE(1, 16) TC_CASE(1, 32) TC_CASE(1, 64) TC_CASE(2, 32) TC_CASE(2, 64)
 #undef TC_CASE
     return cudaErrorInvalidValue;

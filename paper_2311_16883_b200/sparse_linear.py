@@ -50,8 +50,8 @@ class _SparseLinearFn(torch.autograd.Function):
         dw = None
         if ctx.needs_input_grad[1]:
             dy_w = dy.to(torch.bfloat16) if ctx.prec == "bf16" and dy.dtype != torch.bfloat16 else dy
-            # dW = X_bsr^T . dY is K x N; nn.Linear stores weight as N x K
-            dw = wgrad(bsr, dy_w, prec=ctx.prec).t().to(weight.dtype)
+            # nn.Linear stores weight as N x K: the library writes dW^T directly (bsr_wgrad_nk)
+            dw = wgrad(bsr, dy_w, prec=ctx.prec, layout="nk").to(weight.dtype)
         db = dy.sum(0) if ctx.has_bias and ctx.needs_input_grad[2] else None
         ctx.bsr = None
         return dx, dw, db, None, None, None

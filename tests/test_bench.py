@@ -52,6 +52,16 @@ def test_native_arm_c4_one_gpu():
 
 
 @pytest.mark.gpu
+def test_native_arm_c3_whole_s12():
+    """--config C3 (BASELINE configs[2]): all 12 x (fc1, fc2) linear layers of
+    ResMLP-S12 at batch 128, fp32 activations, FP32-grade dW."""
+    d = run_bench("--config", "C3", "--steps", "3", "--warmup", "3", timeout=900)
+    assert d["config"]["rows_per_rank"] == 128 * 196 and d["config"]["dw_prec"] == "fp32"
+    assert d["gpu_launches_per_step"] >= 24 * 3
+    assert d["value"] > 0 and d["ms_per_step"] > 0 and "S12" in d["config"]["workload"]
+
+
+@pytest.mark.gpu
 def test_native_arm_two_ranks_control_flow():
     """--gpus 2 re-launches itself under torch.distributed.run; with the gloo test hook
     both ranks share the one GPU, which exercises the N > 1 control flow (barriers,
