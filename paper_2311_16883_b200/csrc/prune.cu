@@ -1171,7 +1171,8 @@ static cudaError_t launch_prune_t(PruneParams p, cudaStream_t stream, void *ws, 
     }
     // (no per-launch memset: the kernels leave their workspace header zeroed, see above)
     cudaError_t e = cudaSuccess;
-    if (p.N <= kSmallN) return launch_small_t<ES, B, false>(p, StochArgs{0, 0.0, 0ull}, stream);
+    if (p.N <= kSmallN && small_smem_bytes(p.N, p.units, 0) <= kSmallSmemMax)
+        return launch_small_t<ES, B, false>(p, StochArgs{0, 0.0, 0ull}, stream);
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, prune_kernel<ES, B>, kThreads, 0);
     if (e != cudaSuccess) return e;
