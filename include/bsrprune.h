@@ -196,8 +196,10 @@ BSR_API bsr_status_t bsr_prune_k(const void *X, int64_t M, int64_t K, int32_t b,
  * window: >= 0 with min(window, k, N - k) <= 4096 (else BSR_ERR_INVALID_ARG);
  * p in [0, 1].  Outputs as bsr_prune_k.  ws: bsr_prune_stochastic_workspace_bytes
  * bytes (a bsr_prune workspace of the same shape extended; zero-filled before
- * first use and left zero-filled).  Stream-ordered, 9 kernels, no host sync,
- * CUDA-graph capturable. */
+ * first use and left zero-filled).  Stream-ordered, no host sync, CUDA-graph
+ * capturable: 2 kernels while every CTA can hold all N keys and the 2w boundary
+ * blocks in shared memory (N up to ~43K keys), else 9 (global dual radix select,
+ * cooperative marking and packing, one-CTA sort of the boundary). */
 BSR_API size_t bsr_prune_stochastic_workspace_bytes(int64_t M, int64_t K, int32_t b);
 BSR_API bsr_status_t bsr_prune_stochastic(const void *X, int64_t M, int64_t K, int32_t b, int64_t k,
                                   int64_t window, double p, uint64_t seed, int32_t dtype, bsr_t *out,

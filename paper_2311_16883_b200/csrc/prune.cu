@@ -1338,7 +1338,9 @@ cudaError_t launch_prune_threshold(const void *X, int64_t M, int64_t K, int b, i
 //   ranks [A, B)      the boundary: pair i (rank k-1-i, rank k+i) swaps iff
 //                     u_i < p, u_i = splitmix64(seed, i) as a 53-bit uniform,
 //   ranks [B, N)      pruned.
-// Kernels (stream order, 9 launches, graph-capturable):
+// While every CTA can hold all keys and the boundary list in shared memory, the
+// small-N pair (prune_sums_kernel + prune_finish_kernel<STOCH = true>) does it in
+// two launches.  Beyond that (stream order, 9 launches, graph-capturable):
 //   prune_sums_kernel  block sums + digit-0 histogram (shared with bsr_prune)
 //   stoch_update x3 / stoch_hist x2   radix select of ranks A and B together
 //   stoch_mark (coop)  flat-order tie scan: slot[f] = 1 for ranks < A, the
