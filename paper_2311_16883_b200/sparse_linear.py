@@ -57,14 +57,17 @@ class _SparseLinearFn(torch.autograd.Function):
         return dx, dw, db, None, None, None
 
 
-def _default_prec(dtype: torch.dtype, block: int, out_features: int) -> str:
+def _default_prec(dtype: torch.dtype, block: int, out_features: int, rows: int = 0, in_features: int = 0) -> str:
     """dW arithmetic matching what nn.Linear would give: fp32 activations get the
     FP32-grade path (rel-F <= 1e-5: 3xTF32 tensor cores where the library has them,
-    FFMA otherwise -- the library picks), bf16 activations the bf16 tensor-core
-    path where it exists (b >= 16, N % 128 == 0) and the FP32 FFMA path (which
-    reads bf16 storage) elsewhere."""
-    if dtype == torch.bfloat16 and block >= 16 and out_features % 128 == 0:
-        return "bf16"
+    FFMA otherwise -- the library picks), bf16 activations the bf16 tensor cores
+    where they apply: N % 128 == 0 and either b >= 16 (the block kernels) or rows
+    and in_features multiples of 32 (b < 16: the dense rebuild of the masked X,
+    measured 3-20x faster than the FFMA kernel on S12 at b = 4/8,
+    profiles/r02g/c3.jsonl); the FP32 FFMA path (which reads bf16 storage) elsewhere."""
+    if dtype == torch.bfloat16 and out_features % 128 == 0:
+        if block >= 16 or (rows % 32 == 0 and in_features % 32 == 0 and rows > 0):
+            return "bf16"
     return "fp32"
 
 
@@ -73,7 +76,7 @@ def sparse_linear(x: torch.Tensor, weight: torch.Tensor, bias=None, sparsity: fl
     """Functional form: y = x W^T + b with the input activation saved as top-k BSR."""
     lead = x.shape[:-1]
     x2d = x.reshape(-1, x.shape[-1]).contiguous()
-    p = prec or _default_prec(x.dtype, block, weight.shape[0])
+    p = prec or _default_prec(x.dtype, block, weight.shape[0], x2d.shape[0], x2d.shape[1])
     y = _SparseLinearFn.apply(x2d, weight, bias, 1.0 - float(sparsity), int(block), p)
     return y.reshape(*lead, weight.shape[0])
 

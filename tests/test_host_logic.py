@@ -174,3 +174,16 @@ def test_gloo_two_ranks_bucketed_allreduce():
         want = res[0][2][i] + res[1][2][i]
         for r in range(world):
             np.testing.assert_allclose(res[r][1][i], want, rtol=1e-15, atol=0)
+
+
+def test_default_prec_choices():
+    """The layer's default dW arithmetic for each storage type and shape."""
+    import torch
+    from paper_2311_16883_b200.sparse_linear import _default_prec
+    f32, bf16 = torch.float32, torch.bfloat16
+    assert _default_prec(f32, 32, 1536, 25088, 384) == "fp32"
+    assert _default_prec(bf16, 32, 1536, 25088, 384) == "bf16"
+    assert _default_prec(bf16, 4, 1536, 25088, 384) == "bf16"    # dense rebuild: 32 | rows, 32 | in
+    assert _default_prec(bf16, 4, 1536, 25080, 384) == "fp32"    # rows not a multiple of 32
+    assert _default_prec(bf16, 8, 200, 25088, 384) == "fp32"     # N not a multiple of 128
+    assert _default_prec(bf16, 16, 200, 25088, 384) == "fp32"

@@ -94,9 +94,10 @@ def test_saved_activation_is_the_bsr():
 
 
 @pytest.mark.parametrize("block", [4, 8])
-def test_bf16_small_blocks_use_fp32_path(block):
-    """bf16 activations with b < 16 (no tensor-core dW at that block size): the
-    layer's default precision must be the FP32 FFMA path, not bf16."""
+def test_bf16_small_blocks(block):
+    """bf16 activations with b < 16: no block tensor-core kernel at that size, so the
+    layer's default is the bf16 dense rebuild where the shape allows it and the FP32
+    FFMA path otherwise -- never a bf16 call the library rejects."""
     layer, x, y, x_np, dy_np = run(None, 0.5, block, N=256, dtype=torch.bfloat16)
     assert layer.weight.grad is not None and torch.isfinite(layer.weight.grad).all()
     xb, dyb = synth.to_bf16_bits(x_np), synth.to_bf16_bits(dy_np)
@@ -118,3 +119,4 @@ def test_fp32_layer_defaults_to_fp32_grade():
     dw_ref = oracle.wgrad(ref["rowptr"], ref["colidx"], ref["values"], M, K, 32, dy_np)
     got = layer.weight.grad.detach().t().cpu().numpy()
     assert oracle.rel_frobenius(got, dw_ref) <= 1e-5
+

@@ -84,10 +84,11 @@ def timed(fn, sets, reps):
 
 
 def prec_for(dtype, b):
-    """bf16 storage: the bf16 tensor cores where they exist; fp32 storage: the FP32
-    grade (3xTF32 tensor cores at b >= 32, FFMA below) -- the library's defaults."""
+    """bf16 storage: the bf16 tensor cores (block kernels at b >= 16, the dense rebuild
+    below); fp32 storage: the FP32 grade (3xTF32 tensor cores at b >= 32, the dense
+    rebuild below) -- the library's defaults."""
     if dtype == torch.bfloat16:
-        return "bf16" if b >= 16 else "fp32"
+        return "bf16"
     return "fp32"
 
 
