@@ -96,6 +96,21 @@ def test_dw_full_elementwise(layer, prec, algo):
     assert (np.abs(got - ref_dW) / scale).max() <= 20 * TOL[prec]
 
 
+@pytest.mark.parametrize("layer", ["C2", "fc2"])
+def test_dw_nk_full(layer):
+    """bsr_wgrad_nk at full size (the FP32-grade native transposing split-K reduce):
+    bit-identical to bsr_wgrad's dW transposed, and against the full oracle."""
+    X, dY, k, b, ref, ref_dW = _layer(layer, False)
+    A = bp.prune(to_torch(X), b, k=k)
+    dYt = to_torch(dY)
+    kn = bp.wgrad(A, dYt, prec="fp32")
+    nk = torch.full((ref_dW.shape[1], ref_dW.shape[0]), float("nan"), device="cuda")
+    bp.wgrad(A, dYt, prec="fp32", layout="nk", out=nk)
+    torch.cuda.synchronize()
+    assert torch.equal(nk, kn.t())
+    assert oracle.rel_frobenius(nk.t().cpu().numpy(), ref_dW) <= TOL["fp32"]
+
+
 # ----------------------------------------------------------------------------- prune / decompress, full size
 @pytest.mark.parametrize("b", [4, 32])
 def test_prune_c5_1gib(b):
