@@ -12,9 +12,11 @@
 //   rows_select_kernel  one CTA per sample: exact radix select (8+8+8+7 bits,
 //                       shared-memory histograms) of the sample's k_s-th key,
 //                       then a flat-order scan gives each kept segment its slot
-//                       s * k_s + rank; it writes colidx, rowptr and copies the
-//                       segment (raw bits) into values.  No grid-wide step: the
-//                       samples' offsets are known (every sample keeps k_s).
+//                       s * k_s + rank; it writes colidx and rowptr.  No grid-wide
+//                       step: the samples' offsets are known (every sample keeps k_s).
+//   rows_pack_kernel    one warp per row over the whole GPU: the kept segments
+//                       gathered from X into values (raw bits) -- the copy used to
+//                       run inside the per-sample CTAs, latency-bound there.
 //   rows_decompress_kernel  one warp per row: zeros, then the kept segments.
 //   rows_wgrad_kernel   dW = X_bsr^T dY (fp32 FFMA, fixed order, deterministic):
 //                       CTA = 128 kcols x 128 dY columns x a range of rows,
@@ -99,7 +101,10 @@ __device__ __forceinline__ uint64_t scan64(uint64_t v, uint64_t *s_warp, uint64_
     return base + x - v;
 }
 
-constexpr int kSmemKeys = 12288;  // a sample's keys staged in shared memory when they fit (48 KB)
+// a sample's keys staged in shared memory when they fit: up to 208 KB (one CTA per
+// SM; the S12 fc1 samples at every b and fc2 at b >= 8 fit; measured 12288 -> this:
+// profiles/r02h/rows_*.json)
+constexpr int kSmemKeys = 53248;
 
 template <int ES, int B>
 __global__ void __launch_bounds__(kThreads) rows_select_kernel(const uint8_t *__restrict__ X, int64_t K, int64_t S,
@@ -138,9 +143,18 @@ __global__ void __launch_bounds__(kThreads) rows_select_kernel(const uint8_t *__
             const int w = pass < 3 ? 8 : 7, nshift = shift - w;
             if (threadIdx.x < 256) s_h[threadIdx.x] = 0;
             __syncthreads();
-            for (int64_t fb = 0; fb < ns; fb += kThreads) {
-                const int64_t f = fb + threadIdx.x;
-                const uint32_t key = f < ns ? key_of(keyat(f)) : 0u;
+            for (int64_t fb0 = 0; fb0 < ns; fb0 += 4 * kThreads) {
+              float kv[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                  const int64_t f = fb0 + u * kThreads + threadIdx.x;
+                  kv[u] = f < ns ? keyat(f) : 0.f;  // 4 independent loads in flight (keys off chip)
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int64_t f = fb0 + u * kThreads + threadIdx.x;
+                if (fb0 + u * kThreads >= ns) break;
+                const uint32_t key = f < ns ? key_of(kv[u]) : 0u;
                 const bool in = f < ns && (pass == 0 || (key >> shift) == prefix);
                 const uint32_t bin = (key >> nshift) & ((1u << w) - 1u);
                 const uint32_t im = __ballot_sync(0xffffffffu, in);
@@ -152,6 +166,7 @@ __global__ void __launch_bounds__(kThreads) rows_select_kernel(const uint8_t *__
                 } else if (in) {
                     atomicAdd(&s_h[bin], 1u);
                 }
+              }
             }
             __syncthreads();
             // bins in descending order: thread t owns bin 255 - t; exclusive scan = keys above
@@ -179,11 +194,14 @@ __global__ void __launch_bounds__(kThreads) rows_select_kernel(const uint8_t *__
     const uint32_t r = need;  // keys == prefix to keep (lowest flat index first)
     // flat-order scan: slots, colidx, rowptr, raw-bit copy of the kept segments
     uint64_t base = 0;
+    float kcur = threadIdx.x < ns ? keyat(threadIdx.x) : 0.f;
     for (int64_t fb = 0; fb < ns; fb += kThreads) {
         const int64_t f = fb + threadIdx.x;
+        // the next chunk's key is in flight while this chunk is scanned (keys off chip)
+        const float knext = f + kThreads < ns ? keyat(f + kThreads) : 0.f;
         uint32_t a = 0, t = 0;
         if (f < ns) {
-            const uint32_t kk = key_of(keyat(f)) >> shift;
+            const uint32_t kk = key_of(kcur) >> shift;
             if (ks == ns) {
                 a = 1;
             } else if (ks > 0) {
@@ -198,21 +216,49 @@ __global__ void __launch_bounds__(kThreads) rows_select_kernel(const uint8_t *__
             const bool kept = a || (t && tb < r);
             const int64_t pos = out0 + ab + min(r, tb);
             const int64_t row = f / nbc, J = f - row * nbc;
-            if (kept) {
-                colidx[pos] = (int32_t)J;
-                const uint8_t *src = X + ((s * S + row) * K + J * B) * ES;
-                uint8_t *dst = values + pos * B * ES;
-                if constexpr (B * ES >= 16) {
-#pragma unroll
-                    for (int q = 0; q < B * ES / 16; ++q)
-                        reinterpret_cast<uint4 *>(dst)[q] = __ldg(reinterpret_cast<const uint4 *>(src) + q);
-                } else {
-                    *reinterpret_cast<uint2 *>(dst) = __ldg(reinterpret_cast<const uint2 *>(src));
-                }
-            }
+            if (kept) colidx[pos] = (int32_t)J;  // the segment itself: rows_pack_kernel
             if (J == nbc - 1) rowptr[s * S + row + 1] = (int32_t)(out0 + ab + a + min(r, tb + t));
         }
         base += tot;
+        kcur = knext;
+    }
+}
+
+// Copy the kept segments into values (raw bits): one warp per row, the row's
+// stored entries [rowptr[r], rowptr[r+1]) gathered from X at colidx -- the
+// inverse of rows_decompress_kernel, over the whole GPU (the select kernel runs
+// one CTA per sample and only indexes).
+template <int ES, int B>
+__global__ void __launch_bounds__(256) rows_pack_kernel(const uint8_t *__restrict__ X, const int32_t *__restrict__ rowptr,
+                                                        const int32_t *__restrict__ colidx, int64_t M, int64_t K,
+                                                        uint8_t *__restrict__ values) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int PC = B * ES >= 16 ? 16 : B * ES, NP = B * ES / PC;
+    for (int64_t r = w0; r < M; r += nw) {
+        const int a = __ldg(rowptr + r), z = __ldg(rowptr + r + 1);
+        for (int i0 = lane; i0 < (z - a) * NP; i0 += 4 * 32) {  // 4 segments' pieces in flight per lane
+            uint4 v[4];
+            uint8_t *dst[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * 32;
+                dst[u] = nullptr;
+                if (i < (z - a) * NP) {
+                    const int e = a + i / NP, q = i % NP;
+                    const uint8_t *src = X + (r * K + (int64_t)__ldg(colidx + e) * B) * ES + q * PC;
+                    dst[u] = values + (int64_t)e * B * ES + q * PC;
+                    if constexpr (PC == 16) v[u] = __ldcs(reinterpret_cast<const uint4 *>(src));
+                    else { const uint2 t = __ldcs(reinterpret_cast<const uint2 *>(src)); v[u] = make_uint4(t.x, t.y, 0, 0); }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (!dst[u]) continue;
+                if constexpr (PC == 16) __stcs(reinterpret_cast<uint4 *>(dst[u]), v[u]);
+                else __stcs(reinterpret_cast<uint2 *>(dst[u]), make_uint2(v[u].x, v[u].y));
+            }
+        }
     }
 }
 
@@ -449,6 +495,12 @@ cudaError_t launch_prune_rows(const void *X, int64_t M, int64_t K, int b, int es
         rows::rows_select_kernel<ES_, B_><<<(unsigned)(M / S), rows::kThreads, smem_, stream>>>(                   \
             static_cast<const uint8_t *>(X), K, S, ks, sumsq, rowptr, colidx, static_cast<uint8_t *>(values));     \
         count_launch();                                                                                           \
+        if (ks > 0) {                                                                                             \
+            const unsigned g3 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((M + 7) / 8, (int64_t)rows::sms() * 16)); \
+            rows::rows_pack_kernel<ES_, B_><<<g3, 256, 0, stream>>>(static_cast<const uint8_t *>(X), rowptr, colidx, \
+                                                                  M, K, static_cast<uint8_t *>(values));          \
+            count_launch();                                                                                       \
+        }                                                                                                         \
         return cudaGetLastError();                                                                                \
     }())
     if (es == 4) {

@@ -137,12 +137,13 @@ def test_rows_selection_full_s12_batch():
     np.testing.assert_array_equal(A.values.cpu().numpy().view(np.int32), ref["values"].reshape(-1, b).view(np.int32))
 
 
-@pytest.mark.parametrize("S,K,b", [(128, 384, 4), (128, 768, 8)])
+@pytest.mark.parametrize("S,K,b", [(128, 384, 4), (128, 768, 8), (416, 512, 4), (208, 2048, 8), (196, 1536, 4)])
 def test_rows_select_keys_at_shared_memory_limit(S, K, b):
-    """A sample of exactly 12288 segment keys (48 KB, the on-chip threshold): the
-    select kernel's dynamic shared memory plus its static arrays exceed the
-    default 48 KB limit, so the launch must opt in."""
-    assert S * K // b == 12288
+    """Samples of 12288 segment keys (48 KB: beyond the default dynamic shared
+    memory limit, so the launch must opt in -- ADVICE r01), exactly 53248 (208 KB,
+    the on-chip threshold) and 75264 (S12 fc2 at b = 4: the keys stay in global
+    memory, 4 loads in flight per thread)."""
+    assert S * K // b in (12288, 53248, 75264)
     M = 2 * S
     X = synth.ints(M, K, 77)  # exact sums; ties decided by the flat-index rule
     ks = oracle.keep_count(S * K // b, 0.5)
