@@ -192,7 +192,42 @@ __global__ void __launch_bounds__(kThreads) rows_select_kernel(const uint8_t *__
         need = ks == 0 ? 0u : (uint32_t)ns;
     }
     const uint32_t r = need;  // keys == prefix to keep (lowest flat index first)
-    // flat-order scan: slots, colidx, rowptr, raw-bit copy of the kept segments
+    auto flags = [&](float key, uint32_t &a, uint32_t &t) {
+        const uint32_t kk = key_of(key) >> shift;
+        a = ks == ns ? 1u : ks > 0 ? (uint32_t)(kk > prefix) : 0u;
+        t = (ks > 0 && ks < ns) ? (uint32_t)(kk == prefix) : 0u;
+    };
+    if (on_chip) {
+        // keys on chip: thread-contiguous chunks (c odd: conflict-free), one block scan
+        // of the per-thread (above, tie) counts, then each thread walks its chunk
+        // again -- instead of one block-wide scan per 512 keys
+        const int64_t c = ((ns + kThreads - 1) / kThreads) | 1;
+        const int64_t t0 = ns < (int64_t)threadIdx.x * c ? ns : (int64_t)threadIdx.x * c;
+        const int64_t t1 = ns < t0 + c ? ns : t0 + c;
+        uint32_t na = 0, nt = 0;
+        for (int64_t f = t0; f < t1; ++f) {
+            uint32_t a, t;
+            flags(s_keys[f], a, t);
+            na += a;
+            nt += t;
+        }
+        uint64_t tot;
+        const uint64_t ex = scan64(((uint64_t)na << 32) | nt, s_warp, tot);
+        uint32_t ab = (uint32_t)(ex >> 32), tb = (uint32_t)ex;
+        for (int64_t f = t0; f < t1; ++f) {
+            uint32_t a, t;
+            flags(s_keys[f], a, t);
+            const bool kept = a || (t && tb < r);
+            const int64_t pos = out0 + ab + min(r, tb);
+            const int64_t row = f / nbc, J = f - row * nbc;
+            if (kept) colidx[pos] = (int32_t)J;  // the segment itself: rows_pack_kernel
+            if (J == nbc - 1) rowptr[s * S + row + 1] = (int32_t)(out0 + ab + a + min(r, tb + t));
+            ab += a;
+            tb += t;
+        }
+        return;
+    }
+    // keys off chip: flat-order scan in 512-key chunks, the next chunk's keys in flight
     uint64_t base = 0;
     float kcur = threadIdx.x < ns ? keyat(threadIdx.x) : 0.f;
     for (int64_t fb = 0; fb < ns; fb += kThreads) {
