@@ -894,7 +894,12 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
                 const int ab = j % p.na;
                 if (j >= p.na) mbar_wait(aempty + ab, (uint32_t)((j / p.na) - 1) & 1u);
                 tc_fence_after();
-                if constexpr (C::X3) store_slab<2, C::SROWS>(a_tm0 + (uint32_t)(ab * C::A_STEP), v);
+                if constexpr (C::X3) {  // per block row q: hi slab, then its lo slab (A_ROW columns)
+#pragma unroll
+                    for (int q = 0; q < R; ++q)
+                        store_slab<2, B>(a_tm0 + (uint32_t)(ab * C::A_STEP + q * C::A_ROW),
+                                         *reinterpret_cast<const uint32_t(*)[B]>(v + q * B));
+                }
                 else store_slab<KIND, C::SROWS>(a_tm0 + (uint32_t)(ab * C::A_STEP), v);
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 tc_fence_before();
