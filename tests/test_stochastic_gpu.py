@@ -146,3 +146,12 @@ def test_stochastic_small_n_limit_b64():
     h = synth.to_bf16_bits(X)
     compare(h, b, 12288, 4096, 0.5, seed=4, bf16=True)
     compare(h, b, 12288, 1000, 0.5, seed=4, bf16=True)
+
+
+def test_stochastic_large_n_bf16():
+    """The multi-kernel path (N = 150528 keys: S12 fc1 at b = 4) on bf16 storage."""
+    b, M, K = 4, 25088, 384
+    X = synth.ints(M, K, seed=8, lo=-6, hi=6)
+    h = synth.to_bf16_bits(X)
+    N = (M // b) * (K // b)
+    compare(h, b, N // 3, 2048, 0.4, seed=5, bf16=True)
