@@ -210,6 +210,14 @@ BSR_API bsr_status_t bsr_prune_stochastic(const void *X, int64_t M, int64_t K, i
 BSR_API bsr_status_t bsr_block_sumsq(const void *X, int64_t M, int64_t K, int32_t b, int32_t dtype,
                              float *sumsq, void *stream);
 
+/* Structural check of a BSR on the device (the validation hook of SURVEY §5):
+ * rowptr[0] == 0, rowptr non-decreasing, rowptr[M/b] == A->nnzb, and within every
+ * block row colidx strictly ascending and in [0, K/b).  Writes to
+ * *bad_row (caller-owned DEVICE int32) -1 when every row holds, else the lowest
+ * offending block row.  Reads rowptr / colidx only; stream-ordered, no host
+ * sync (3 tiny kernels); the values are not inspected. */
+BSR_API bsr_status_t bsr_validate(const bsr_t *A, int32_t *bad_row, void *stream);
+
 /* Dense M x K matrix (A->dtype) with every stored block at its position and
  * +0.0 elsewhere: X_out == X masked to the kept blocks, bit for bit
  * (SPEC decode; P:L162-168 read backwards).  X_out must hold M*K elements. */

@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from ._lib import ALGO, BsrError, DT_BF16, DT_F32, PREC
 
-__all__ = ["BSR", "BsrError", "prune", "prune_stochastic", "decompress", "wgrad", "block_sumsq", "num_blocks", "keep_count",
+__all__ = ["BSR", "BsrError", "prune", "prune_stochastic", "validate", "decompress", "wgrad", "block_sumsq", "num_blocks", "keep_count",
            "storage_bytes", "workspace", "version", "set_pdl", "wgrad_multicast", "affine_wgrad", "SparseAffine", "SparseLinear", "sparse_linear", "prune_global",
            "RowBSR", "prune_rows", "decompress_rows", "wgrad_rows", "act_prune"]
 
@@ -195,6 +195,17 @@ def prune_stochastic(X: torch.Tensor, b: int, keep: float | None = None, k: int 
     _lib.check(lib.bsr_prune_stochastic(X.data_ptr(), M, K, b, k, int(window), float(p), int(seed) & (2**64 - 1),
                                         _dt(X), ctypes.byref(cs), ws.data_ptr(), ws.numel(), _stream(stream)))
     return out
+
+
+def validate(A: BSR, stream=None) -> int:
+    """Structural check of a BSR on the device (bsr_validate): -1 when rowptr / colidx
+    hold the BSR invariants, else the lowest offending block row.  Reads the result
+    back (one device-to-host copy of an int32)."""
+    lib = _lib.load()
+    bad = torch.empty(1, dtype=torch.int32, device=A.rowptr.device)
+    cs = A.c_struct()
+    _lib.check(lib.bsr_validate(ctypes.byref(cs), bad.data_ptr(), _stream(stream)))
+    return int(bad.item())
 
 
 def act_prune(Z: torch.Tensor, b: int, keep: float | None = None, k: int | None = None, act: str = "gelu",

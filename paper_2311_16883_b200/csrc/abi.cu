@@ -541,6 +541,16 @@ bsr_status_t bsr_prune_presummed(const void *X, int64_t M, int64_t K, int32_t b,
     return prune_impl(X, M, K, b, k, dtype, out, ws, ws_bytes, stream, 1);
 }
 
+bsr_status_t bsr_validate(const bsr_t *A, int32_t *bad_row, void *stream) {
+    bsr_status_t st = check_bsr(A);
+    if (st != BSR_OK) return st;
+    if (!bad_row) return fail(BSR_ERR_INVALID_ARG, "bad_row is NULL");
+    if (A->nnzb > 0 && !A->colidx) return fail(BSR_ERR_INVALID_ARG, "colidx is NULL with nnzb > 0");
+    return cuda_status(bsrp::launch_validate(A->rowptr, A->colidx, A->M / A->b, A->K / A->b, A->nnzb, bad_row,
+                                             static_cast<cudaStream_t>(stream)),
+                       "bsr_validate launch");
+}
+
 bsr_status_t bsr_decompress(const bsr_t *A, void *X_out, void *stream) {
     bsr_status_t st = check_bsr(A);
     if (st != BSR_OK) return st;

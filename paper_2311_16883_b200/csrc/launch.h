@@ -115,6 +115,9 @@ cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const 
 cudaError_t launch_transpose_reduce(const float *ws, float *dWt, int64_t K, int64_t N, int nsplit, int accumulate,
                                     cudaStream_t stream);
 bool wgrad_x3_native_nk(int64_t M, int64_t K, int b, int64_t N);
+// bsr_validate: *bad = -1, or the lowest block row breaking the BSR invariants.
+cudaError_t launch_validate(const int32_t *rowptr, const int32_t *colidx, int64_t nbr, int64_t nbc, int64_t nnzb,
+                            int32_t *bad, cudaStream_t stream);
 
 // Span kernel (wgrad_span.cu): dense-padded per-row spans, CTA-pair MMAs.
 size_t wgrad_span_ws_bytes(int64_t M, int64_t K, int b, int64_t N);

@@ -1286,6 +1286,46 @@ cudaError_t launch_decompress(const int32_t *rowptr, const int32_t *colidx, cons
 #undef CALL
 }
 
+// Structural check of a BSR (bsr_validate): block row r is bad if rowptr[0] != 0
+// (r = 0), rowptr decreases at r, rowptr[nbr] != nnzb (r = nbr - 1), or its colidx
+// entries are not strictly ascending or not in [0, nbc).  bad = the lowest bad row.
+__global__ void validate_init_kernel(int32_t *bad) { *bad = 0x7fffffff; }
+__global__ void __launch_bounds__(256) validate_kernel(const int32_t *__restrict__ rowptr,
+                                                       const int32_t *__restrict__ colidx, int64_t nbr, int64_t nbc,
+                                                       int64_t nnzb, int32_t *bad) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nbr; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t a = rowptr[r], z = rowptr[r + 1];
+        bool ok = a <= z && a >= 0 && z <= nnzb;
+        if (r == 0) ok = ok && a == 0;
+        if (r == nbr - 1) ok = ok && z == nnzb;
+        if (ok) {
+            int32_t prev = -1;
+            for (int32_t e = a; e < z; ++e) {
+                const int32_t c = colidx[e];
+                if (c <= prev || c >= nbc) {
+                    ok = false;
+                    break;
+                }
+                prev = c;
+            }
+        }
+        if (!ok) atomicMin(bad, (int32_t)r);
+    }
+}
+__global__ void validate_finish_kernel(int32_t *bad) {
+    if (*bad == 0x7fffffff) *bad = -1;
+}
+
+cudaError_t launch_validate(const int32_t *rowptr, const int32_t *colidx, int64_t nbr, int64_t nbc, int64_t nnzb,
+                            int32_t *bad, cudaStream_t stream) {
+    validate_init_kernel<<<1, 1, 0, stream>>>(bad);
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nbr + 255) / 256, (int64_t)num_sms() * 8));
+    validate_kernel<<<g, 256, 0, stream>>>(rowptr, colidx, nbr, nbc, nnzb, bad);
+    validate_finish_kernel<<<1, 1, 0, stream>>>(bad);
+    count_launch(3);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_prune_threshold(const void *X, int64_t M, int64_t K, int b, int es, uint32_t T, int shift,
                                    uint32_t tie_take, int64_t k, int32_t *rowptr, int32_t *colidx, void *values,
                                    void *ws, cudaStream_t stream, const uint64_t *gstate) {
