@@ -1022,6 +1022,11 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const void *X, int64_t K, in
     }
 }
 
+// Warps per decompress unit (each copying B / parts rows): more warps in flight for
+// the wide blocks, whose units are 16 KB (fp32) of output each.
+template <int B>
+constexpr int kDecompRowParts = B >= 32 ? 2 : 1;
+
 // BSR -> dense: every output row segment written once (zeros or the block).
 // The warp's unit covers G consecutive block columns of one block row; the
 // row's stored columns are scanned 32 at a time with one coalesced colidx load
@@ -1037,12 +1042,16 @@ __global__ void __launch_bounds__(256) decompress_kernel(const int32_t *__restri
     using G_ = Geo<ES, B>;
     using V = typename G_::V;
     constexpr int RD = (B < 16) ? B : 16;
+    constexpr int RS = kDecompRowParts<B>;  // warps per unit, each copying B / RS rows
+    constexpr int BR = B / RS;
     __shared__ int s_pos[256 / 32][G_::G];  // B >= 16 lookup slots
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int j = lane / G_::LPB, sub = lane % G_::LPB;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t u = wg; u < units; u += nwg) {
+    for (int64_t task = wg; task < units * RS; task += nwg) {
+        const int64_t u = task / RS;
+        const int part = (int)(task - u * RS);
         const int64_t I = u / upr;
         const int Jb = (int)((u % upr) * G_::G);
         const int64_t J = Jb + j;
@@ -1075,21 +1084,22 @@ __global__ void __launch_bounds__(256) decompress_kernel(const int32_t *__restri
         }
         if (J >= nbc) continue;
         const int64_t rs = K / G_::EPV;
-        V *dst = reinterpret_cast<V *>(Xout) + (I * B) * rs + (J * B) / G_::EPV + sub;
+        V *dst = reinterpret_cast<V *>(Xout) + (I * B + part * BR) * rs + (J * B) / G_::EPV + sub;
         if (lo >= 0) {
-            const V *src = reinterpret_cast<const V *>(values) + (int64_t)lo * (B * B / G_::EPV) + sub;
+            const V *src = reinterpret_cast<const V *>(values) + (int64_t)lo * (B * B / G_::EPV) + part * BR * G_::LPB + sub;
+            constexpr int RDP = RD < BR ? RD : BR;
 #pragma unroll
-            for (int r0 = 0; r0 < B; r0 += RD) {
-                V v[RD];
+            for (int r0 = 0; r0 < BR; r0 += RDP) {
+                V v[RDP];
 #pragma unroll
-                for (int rr = 0; rr < RD; ++rr) v[rr] = ld_stream(src + (r0 + rr) * G_::LPB);
+                for (int rr = 0; rr < RDP; ++rr) v[rr] = ld_stream(src + (r0 + rr) * G_::LPB);
 #pragma unroll
-                for (int rr = 0; rr < RD; ++rr) __stcs(dst + (r0 + rr) * rs, v[rr]);
+                for (int rr = 0; rr < RDP; ++rr) __stcs(dst + (r0 + rr) * rs, v[rr]);
             }
         } else {
             V z{};
 #pragma unroll 8
-            for (int r = 0; r < B; ++r) __stcs(dst + r * rs, z);
+            for (int r = 0; r < BR; ++r) __stcs(dst + r * rs, z);
         }
     }
 }
@@ -1272,7 +1282,7 @@ cudaError_t launch_decompress(const int32_t *rowptr, const int32_t *colidx, cons
     const int64_t nbr = M / b, nbc = K / b;
 #define CALL(ES_, B_) ([&]() {                                                                   \
         int64_t upr = units_per_row<ES_, B_>(nbc), units = nbr * upr;                          \
-        int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((units + 7) / 8, 148 * 16));      \
+        int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((units * kDecompRowParts<B_> + 7) / 8, 148 * 16)); \
         cudaError_t e_ = launch_pdl(pdl_flags() & 64, decompress_kernel<ES_, B_>, dim3((unsigned)blocks), dim3(256), 0, stream, \
                                     rowptr, colidx, values, K, nbc, units, upr, Xout);                    \
         count_launch();                                                                        \
