@@ -275,6 +275,15 @@ BSR_API bsr_status_t bsr_wgrad_nk(const bsr_t *A, const void *dY, int32_t dy_dty
 BSR_API bsr_status_t bsr_wgrad_multicast(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *mc_dW,
                                          int32_t prec, int32_t algo, void *ws, size_t ws_bytes, void *stream);
 
+/* Test hook for the fused reduction of bsr_wgrad_multicast on hardware without a
+ * multicast object (a single-GPU slice): the same kernels, the same addresses and
+ * the same per-element reduction, with red.global.add (device-scope atomics) into
+ * the plain device buffer dW_red instead of multimem.red into a multicast address.
+ * dW_red (+)= dW; the order of the adds across tiles is not fixed. */
+BSR_API bsr_status_t bsr_wgrad_multicast_unicast_test(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N,
+                                              float *dW_red, int32_t prec, int32_t algo, void *ws,
+                                              size_t ws_bytes, void *stream);
+
 /* Programmatic-dependent-launch mask of this process (bit meanings in
  * csrc/launch.h; 0 = plain stream order).  Returns the previous mask.  Results
  * are bit-identical for every mask (tests/test_pdl_gpu.py); only the overlap

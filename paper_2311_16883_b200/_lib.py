@@ -21,7 +21,7 @@ ALGO = {"auto": 0, "runs": 1, "span": 2, "simt": 3, "dense": 4}
 
 EXPORTED = ["bsr_num_blocks", "bsr_keep_count", "bsr_storage_bytes", "bsr_prune_workspace_bytes",
             "bsr_wgrad_workspace_bytes", "bsr_wgrad_algo_workspace_bytes", "bsr_prune", "bsr_prune_k", "bsr_validate", "bsr_prune_stochastic_workspace_bytes", "bsr_prune_stochastic", "bsr_block_sumsq", "bsr_decompress",
-            "bsr_wgrad", "bsr_wgrad_algo", "bsr_wgrad_nk_workspace_bytes", "bsr_wgrad_nk", "bsr_wgrad_multicast", "bsr_set_pdl", "bsr_affine_wgrad_workspace_bytes", "bsr_affine_wgrad", "bsr_select_hist", "bsr_select_counts", "bsr_prune_threshold", "bsr_gselect_state_bytes", "bsr_gselect_init",
+            "bsr_wgrad", "bsr_wgrad_algo", "bsr_wgrad_nk_workspace_bytes", "bsr_wgrad_nk", "bsr_wgrad_multicast", "bsr_wgrad_multicast_unicast_test", "bsr_set_pdl", "bsr_affine_wgrad_workspace_bytes", "bsr_affine_wgrad", "bsr_select_hist", "bsr_select_counts", "bsr_prune_threshold", "bsr_gselect_state_bytes", "bsr_gselect_init",
             "bsr_gselect_hist", "bsr_gselect_update", "bsr_gselect_counts", "bsr_gselect_take", "bsr_prune_gselect", "bsr_rows_keep_per_sample", "bsr_prune_rows_workspace_bytes", "bsr_prune_rows",
             "bsr_decompress_rows", "bsr_wgrad_rows_workspace_bytes", "bsr_wgrad_rows", "bsr_wgrad_rows_tc_workspace_bytes", "bsr_wgrad_rows_tc", "bsr_act_block_sumsq", "bsr_prune_presummed", "bsr_status_string", "bsr_last_error", "bsr_kernel_launches", "bsr_version"]
 
@@ -72,6 +72,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "bsr_wgrad_nk_workspace_bytes": (sz, [i64, i64, i32, i64, i32, i32]),
         "bsr_wgrad_nk": (i32, [P, vp, i32, i64, vp, i32, i32, i32, vp, sz, vp]),
         "bsr_wgrad_multicast": (i32, [P, vp, i32, i64, vp, i32, i32, vp, sz, vp]),
+        "bsr_wgrad_multicast_unicast_test": (i32, [P, vp, i32, i64, vp, i32, i32, vp, sz, vp]),
         "bsr_set_pdl": (ctypes.c_uint32, [ctypes.c_uint32]),
         "bsr_affine_wgrad_workspace_bytes": (sz, [i64, i64, i32]),
         "bsr_affine_wgrad": (i32, [P, vp, i32, vp, i32, vp, sz, vp]),

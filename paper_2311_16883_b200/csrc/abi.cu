@@ -690,8 +690,9 @@ bsr_status_t bsr_wgrad(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t
     return bsr_wgrad_algo(A, dY, dy_dtype, N, dW, accumulate, prec, BSR_ALGO_AUTO, ws, ws_bytes, stream);
 }
 
-bsr_status_t bsr_wgrad_multicast(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *mc_dW,
-                                 int32_t prec, int32_t algo, void *ws, size_t ws_bytes, void *stream) {
+static bsr_status_t wgrad_multicast_impl(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *mc_dW,
+                                         int32_t prec, int32_t algo, void *ws, size_t ws_bytes, void *stream,
+                                         int unicast) {
     bsr_status_t st = check_bsr(A);
     if (st != BSR_OK) return st;
     const int esy = elem_size(dy_dtype);
@@ -714,8 +715,20 @@ bsr_status_t bsr_wgrad_multicast(const bsr_t *A, const void *dY, int32_t dy_dtyp
         return fail(BSR_ERR_WORKSPACE, "workspace of %zu bytes given, %zu needed", ws ? ws_bytes : (size_t)0, need);
     if (need && !aligned16(ws)) return fail(BSR_ERR_ALIGNMENT, "workspace is not 16-byte aligned");
     return cuda_status(bsrp::launch_wgrad_tc(A->rowptr, A->colidx, A->values, A->nnzb, kind, BSR_ALGO_TC_RUNS, A->M,
-                                             A->K, A->b, dY, N, nullptr, 1, ws, static_cast<cudaStream_t>(stream), mc_dW),
+                                             A->K, A->b, dY, N, nullptr, 1, ws, static_cast<cudaStream_t>(stream), mc_dW,
+                                             0, unicast),
                        "bsr_wgrad_multicast launch");
+}
+
+bsr_status_t bsr_wgrad_multicast(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N, float *mc_dW,
+                                 int32_t prec, int32_t algo, void *ws, size_t ws_bytes, void *stream) {
+    return wgrad_multicast_impl(A, dY, dy_dtype, N, mc_dW, prec, algo, ws, ws_bytes, stream, 0);
+}
+
+bsr_status_t bsr_wgrad_multicast_unicast_test(const bsr_t *A, const void *dY, int32_t dy_dtype, int64_t N,
+                                              float *dW_red, int32_t prec, int32_t algo, void *ws, size_t ws_bytes,
+                                              void *stream) {
+    return wgrad_multicast_impl(A, dY, dy_dtype, N, dW_red, prec, algo, ws, ws_bytes, stream, 1);
 }
 
 uint32_t bsr_set_pdl(uint32_t mask) { return bsrp::g_pdl.exchange(mask); }

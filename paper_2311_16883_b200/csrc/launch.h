@@ -110,7 +110,7 @@ bool wgrad_tc_supported(int kind, int algo, int b, int64_t K, int64_t N);
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values,
                             int64_t nnzb, int kind, int algo, int64_t M, int64_t K, int b, const void *dY,
                             int64_t N, float *dW, int accumulate, void *ws, cudaStream_t stream,
-                            float *mc = nullptr, int nk = 0);
+                            float *mc = nullptr, int nk = 0, int mc_unicast = 0);
 // dW^T (N x K) (+)= sum over nsplit K x N partials in ws, in split order (BSR_DW_NK layout).
 cudaError_t launch_transpose_reduce(const float *ws, float *dWt, int64_t K, int64_t N, int nsplit, int accumulate,
                                     cudaStream_t stream);

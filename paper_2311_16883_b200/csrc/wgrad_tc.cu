@@ -265,6 +265,7 @@ struct Params {
     const uint8_t *values;
     float *dW, *ws;
     float *mc;                   // multimem (NVLS multicast) address of the summed dW, or null
+    int mc_unicast;              // 1: mc is a plain device address, reduced with red.global (test hook)
     int64_t nbr, N, K;
     int nkr, nsplit, kr_blocks;  // kcol range = kr_blocks blocks
     int nbslots, na, mode;       // B-ring block slots, TMEM A buffers; mode: 0 store, 1 reduce-add, 3 partial -> ws[split],
@@ -948,8 +949,13 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
                     if (i >= nrow) break;
                     float x = __uint_as_float(v[i]);
                     if constexpr (C::X3) x = __fadd_rn(x, __uint_as_float(w[i]));
-                    asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(dst + (int64_t)i * p.N), "f"(x)
-                                 : "memory");
+                    if (p.mc_unicast)
+                        asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(dst + (int64_t)i * p.N), "f"(x)
+                                     : "memory");
+                    else
+                        asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(dst + (int64_t)i * p.N),
+                                     "f"(x)
+                                     : "memory");
                 }
                 continue;
             }
@@ -1002,7 +1008,7 @@ __global__ void __launch_bounds__(Cfg<KIND, B>::THREADS, 1)
 // registers: 4 CTAs per SM, so the C2 grid (576 CTAs) runs in one wave.
 __global__ void __launch_bounds__(256, 4) splitk_reduce_kernel(const float4 *__restrict__ ws, float4 *__restrict__ dW,
                                                                int64_t n4, int nsplit, int accumulate, int trig,
-                                                               float4 *__restrict__ mc) {
+                                                               float4 *__restrict__ mc, int mc_unicast) {
     if (trig) pdl_trigger();
     pdl_wait();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1018,7 +1024,13 @@ __global__ void __launch_bounds__(256, 4) splitk_reduce_kernel(const float4 *__r
                     a.x += v[u].x; a.y += v[u].y; a.z += v[u].z; a.w += v[u].w;
                 }
         }
-        if (mc)  // fused all-reduce: the split sum is added into the multicast dW (NVSwitch reduction)
+        if (mc && mc_unicast) {  // test hook: the same reduction into a plain device address
+            float *m = reinterpret_cast<float *>(mc + i);
+            atomicAdd(m, a.x);
+            atomicAdd(m + 1, a.y);
+            atomicAdd(m + 2, a.z);
+            atomicAdd(m + 3, a.w);
+        } else if (mc)  // fused all-reduce: the split sum is added into the multicast dW (NVSwitch reduction)
             asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc + i), "f"(a.x),
                          "f"(a.y), "f"(a.z), "f"(a.w)
                          : "memory");
@@ -1117,7 +1129,7 @@ static Plan plan_for(int64_t M, int64_t K, int64_t N, int sms) {
 template <int KIND, int B>
 static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
                             int64_t M, int64_t K, const void *dY, int64_t N, float *dW, int accumulate,
-                            float *ws, cudaStream_t stream, float *mc, int nk) {
+                            float *ws, cudaStream_t stream, float *mc, int nk, int mc_unicast) {
     using C = Cfg<KIND, B>;
     int dev = 0, sms = kSplitSMs;
     cudaGetDevice(&dev);
@@ -1173,6 +1185,7 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     p.chunk_steps = pl.chunk_steps;
     p.ws = ws;
     p.mc = mc;
+    p.mc_unicast = mc_unicast;
     p.mode = pl.nsplit > 1 ? 3 : mc ? 4 : accumulate ? 1 : 0;
     p.pdl_trig = (pdl_flags() & 2) ? 1 : (pdl_flags() & 4) ? 2 : 0;
     auto kern = wgrad_tc_kernel<KIND, B>;
@@ -1189,7 +1202,7 @@ static cudaError_t launch_t(const int32_t *rowptr, const int32_t *colidx, const 
     const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 4));
     e = launch_pdl(pdl_flags() & 32, splitk_reduce_kernel, dim3(rgrid), dim3(256), 0, stream, reinterpret_cast<const float4 *>(ws),
                    reinterpret_cast<float4 *>(dW), n4, (int)pl.nsplit, mc ? 0 : accumulate, (pdl_flags() & 8) ? 1 : 0,
-                   reinterpret_cast<float4 *>(mc));
+                   reinterpret_cast<float4 *>(mc), mc_unicast);
     count_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -1236,7 +1249,7 @@ cudaError_t launch_splitk_reduce(const float *ws, float *dW, int64_t n, int nspl
     const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 4));
     cudaError_t e = launch_pdl(pdl_flags() & 32, tc::splitk_reduce_kernel, dim3(rgrid), dim3(256), 0, stream,
                                reinterpret_cast<const float4 *>(ws), reinterpret_cast<float4 *>(dW), n4, nsplit,
-                               accumulate, (pdl_flags() & 8) ? 1 : 0, static_cast<float4 *>(nullptr));
+                               accumulate, (pdl_flags() & 8) ? 1 : 0, static_cast<float4 *>(nullptr), 0);
     count_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -1321,7 +1334,7 @@ bool wgrad_tc_supported(int kind, int algo, int b, int64_t K, int64_t N) {
 
 cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const void *values, int64_t nnzb,
                             int kind, int algo, int64_t M, int64_t K, int b, const void *dY, int64_t N, float *dW,
-                            int accumulate, void *ws, cudaStream_t stream, float *mc, int nk) {
+                            int accumulate, void *ws, cudaStream_t stream, float *mc, int nk, int mc_unicast) {
     if ((mc || nk) && !use_runs_kernel(kind, algo, b, K)) return cudaErrorNotSupported;  // per-run kernel only
     if (!use_runs_kernel(kind, algo, b, K))
         return launch_wgrad_span(rowptr, colidx, values, nnzb, kind, M, K, b, dY, N, dW, accumulate, ws, stream);
@@ -1331,7 +1344,7 @@ cudaError_t launch_wgrad_tc(const int32_t *rowptr, const int32_t *colidx, const 
     }
 #define TC_CASE(KD, B_) \
     if (kind == KD && b == B_) return tc::launch_t<KD, B_>(rowptr, colidx, values, nnzb, M, K, dY, N, dW, accumulate, \
-                                                            static_cast<float *>(ws), stream, mc, nk);
+                                                            static_cast<float *>(ws), stream, mc, nk, mc_unicast);
     TC_CASE(0, 32) TC_CASE(0, 64) TC_CASE(1, 16) TC_CASE(1, 32) TC_CASE(1, 64) TC_CASE(2, 32) TC_CASE(2, 64)
 #undef TC_CASE
     return cudaErrorInvalidValue;

@@ -110,3 +110,42 @@ def test_multicast_two_ranks_equals_allreduce():
         assert p.exitcode == 0
     for _, err in res:
         assert err <= 1e-6, err
+
+
+# ----------------------------------------------------------------------------- unicast stand-in
+def _unicast(A, dY, out, prec):
+    lib = bp._lib.load()
+    N = dY.shape[1]
+    p = bp.PREC[prec]
+    ws_bytes = lib.bsr_wgrad_workspace_bytes(A.M, A.K, A.b, N, p)
+    ws = bp.workspace(ws_bytes, dY.device) if ws_bytes else None
+    cs = A.c_struct()
+    bp._lib.check(lib.bsr_wgrad_multicast_unicast_test(
+        __import__("ctypes").byref(cs), dY.data_ptr(), bp._dt(dY), N, out.data_ptr(), p, bp.ALGO["auto"],
+        ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0, bp._stream(None)))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("M", [1024, 25088])  # one split (epilogue reduction) / split-K (the reduce kernel's)
+def test_fused_reduction_path_on_unicast_memory(prec, M):
+    """Runs on every box: the fused-reduction kernels of bsr_wgrad_multicast with
+    device-scope red.add into a plain buffer instead of multimem.red -- the same
+    addresses, tiles and split sums -- so the multicast path's indexing is checked on
+    hardware even where no multicast object can be made.  base + dW, twice."""
+    K, N, b = 384, 256, 32
+    bf = prec == "bf16"
+    X = synth.f_aff(M, K, seed=M + 1)
+    dY = synth.grad_out(M, N, M + 2)
+    if bf:
+        Xt, dYt = to_torch(synth.to_bf16_bits(X), bf16=True), to_torch(synth.to_bf16_bits(dY), bf16=True)
+    else:
+        Xt, dYt = to_torch(X), to_torch(dY)
+    A = bp.prune(Xt, b, keep=0.5)
+    dW = bp.wgrad(A, dYt, prec=prec)
+    base = torch.randn(K, N, device="cuda")
+    out = base.clone()
+    _unicast(A, dYt, out, prec)
+    _unicast(A, dYt, out, prec)
+    torch.cuda.synchronize()
+    want = base + 2 * dW
+    torch.testing.assert_close(out, want, rtol=1e-5, atol=1e-5 * float(dW.abs().max()))
